@@ -1,0 +1,130 @@
+/*
+ * ftb.h — C ABI of the B200-native FTuner hot path (libftb.so).
+ *
+ * The reference (mktune 0.1.0, /root/reference/pkg/src/mktune) is a pure
+ * Python package with no FFI. These entry points are what a ctypes/cffi
+ * binding of that package's hot path binds instead; each one names the
+ * reference interface it replaces. Conventions:
+ *   - every function returns an ftb_status; 0 = success;
+ *   - status codes map 1:1 onto mktune.errors (errors.py:10-47):
+ *       FTB_INPUT_ERROR -> InputError, FTB_CAPACITY_ERROR -> CapacityError,
+ *       FTB_EMPTY_RESULT -> EmptyResultError, FTB_MISSING_METRICS ->
+ *       MissingMetricsError, FTB_INTERNAL_ERROR -> InternalError;
+ *     FTB_CUDA_ERROR is new (device failures have no reference analogue);
+ *   - the message of the last failure on the calling thread is returned by
+ *     ftb_last_error();
+ *   - buffers are caller-owned; handles (ftb_exec*, ftb_planner*) are owned by
+ *     the library and released with the matching *_destroy call;
+ *   - no torch types: device pointers are plain void*, streams are the
+ *     cudaStream_t value cast to void*.
+ */
+#ifndef FTB_H_
+#define FTB_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef int32_t ftb_status;
+enum {
+  FTB_OK = 0,
+  FTB_INPUT_ERROR = 2,      /* errors.py:14-22 InputError (exit code 2)          */
+  FTB_EMPTY_RESULT = 1,     /* errors.py:29-39 EmptyResultError (exit code 1)    */
+  FTB_INTERNAL_ERROR = 3,   /* errors.py:46-47 InternalError (exit code 3)       */
+  FTB_CAPACITY_ERROR = 4,   /* errors.py:25-26 CapacityError                     */
+  FTB_MISSING_METRICS = 5,  /* errors.py:42-43 MissingMetricsError              */
+  FTB_CUDA_ERROR = 6        /* new: CUDA runtime / driver failure                */
+};
+
+/* Thread-local message of the last failing call (NUL-terminated, truncated). */
+size_t ftb_last_error(char* buf, size_t n);
+/* Optional: the field name attached to the last InputError (errors.py:20-22). */
+size_t ftb_last_error_field(char* buf, size_t n);
+
+/* ------------------------------------------------------------------------ */
+/* Program (compose/select output)                                          */
+/* ------------------------------------------------------------------------ */
+
+/* Axis order follows the operator spec: space axes then reduce axes.
+ *   Dense: (i, j, k)        C[i,j]   = sum_k A[i,k] B[k,j]
+ *   BMM  : (b, i, j, k)     C[b,i,j] = sum_k A[b,i,k] B[b,k,j]
+ * A program is the reference's ProgramPlan (combine.py:30-55): one or two
+ * uKernels, each with a repetition count along the main axis tau; non-tau
+ * tiles are uniform across parts (combine.py:118-123). */
+#define FTB_MAX_AXES 8
+typedef struct {
+  int32_t n_space;                    /* 2 (dense) or 3 (bmm)                    */
+  int32_t n_reduce;                   /* 1                                       */
+  int32_t tau;                        /* index of tau among the space axes       */
+  int32_t n_parts;                    /* 1 or 2                                  */
+  int64_t reg[2][FTB_MAX_AXES];       /* register tiles (space axes)             */
+  int64_t smem[2][FTB_MAX_AXES];      /* shared-memory tiles (space + reduce)    */
+  int64_t count[2];                   /* repetitions along tau                   */
+  double sia;                         /* score attached by ranking (scoring.py:126) */
+} ftb_program;
+
+/* ------------------------------------------------------------------------ */
+/* Execution (the reference has none: SPEC.md:8 — this is the new L6)       */
+/* ------------------------------------------------------------------------ */
+
+enum { FTB_OP_DENSE = 0, FTB_OP_BMM = 1 };
+enum { FTB_B_KN = 0, /* B stored [K,N], N contiguous (MN-major operand)  */
+       FTB_B_NK = 1  /* B stored [N,K], K contiguous (K-major, nn.Linear) */ };
+enum { FTB_DT_BF16 = 0, FTB_DT_F32 = 1 };
+
+/* One GEMM problem bound to device buffers. Strides are in elements.
+ * Batch strides are ignored for dense (batch = 1). The tcgen05 path needs
+ * bf16 A/B with 16-byte aligned row strides (lda, ldb multiples of 8). */
+typedef struct {
+  int32_t op;            /* FTB_OP_DENSE / FTB_OP_BMM                      */
+  int32_t batch;         /* b (1 for dense)                                */
+  int64_t M, N, K;
+  const void* A; int64_t lda; int64_t a_batch_stride;   /* A[b][M][lda]    */
+  const void* B; int64_t ldb; int64_t b_batch_stride;   /* see b_layout    */
+  void* C;       int64_t ldc; int64_t c_batch_stride;   /* C[b][M][ldc]    */
+  int32_t b_layout;      /* FTB_B_KN / FTB_B_NK                            */
+  int32_t in_dtype;      /* FTB_DT_BF16 (tcgen05) / FTB_DT_F32 (FFMA mode) */
+  int32_t out_dtype;     /* FTB_DT_BF16 / FTB_DT_F32                       */
+  int32_t orientation;   /* -1 auto, 0 lanes=i (normal), 1 lanes=j (swap-AB) */
+} ftb_gemm_desc;
+
+typedef struct ftb_exec ftb_exec;   /* lowered tile-schedule table on device */
+
+typedef struct {
+  int64_t n_work;          /* work items in the table                       */
+  int64_t n_ctas;          /* persistent CTAs launched                      */
+  int64_t n_problems;
+  int64_t mma_flops;       /* flops the tensor cores execute (incl. padding) */
+  int64_t true_flops;      /* 2*b*M*N*K summed                              */
+  int64_t covered_out;     /* output elements covered by the plans          */
+  int64_t true_out;        /* true output elements                          */
+  int32_t kernel;          /* 0 = tcgen05 bf16, 1 = FFMA fp32               */
+} ftb_exec_info;
+
+/* Lower n programs (one per problem) to a tile-schedule table and upload it:
+ * replaces nothing in the reference. The programs must
+ * cover each problem exactly as ProgramPlan.covered_extents (combine.py:44-55)
+ * describes; the table is validated against that before upload. */
+ftb_status ftb_exec_create(const ftb_gemm_desc* problems, const ftb_program* programs,
+                           int32_t n, ftb_exec** out);
+/* Launch the table as one persistent kernel on `stream` (cudaStream_t). */
+ftb_status ftb_exec_launch(ftb_exec* ex, void* stream);
+ftb_status ftb_exec_get_info(const ftb_exec* ex, ftb_exec_info* info);
+/* Host copy of the lowered table (int32 x 8 per work item), for tests. */
+ftb_status ftb_exec_export_table(const ftb_exec* ex, int32_t* out, int64_t cap, int64_t* n_out);
+void ftb_exec_destroy(ftb_exec* ex);
+/* Host-only lowering (no device, no TMA descriptors): the same table
+ * ftb_exec_create would upload, for inspection and CPU tests. */
+ftb_status ftb_lower(const ftb_gemm_desc* problems, const ftb_program* programs, int32_t n,
+                     int32_t* out, int64_t cap, int64_t* n_out, ftb_exec_info* info);
+
+/* Number of SMs of the current device (0 if none). */
+int32_t ftb_device_sm_count(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* FTB_H_ */

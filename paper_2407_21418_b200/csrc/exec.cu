@@ -1,0 +1,391 @@
+// exec.cu — host side of the executor: lowers ProgramPlans to the
+// tile-schedule table, encodes TMA descriptors, uploads, and launches K1/K2.
+//
+// Lowering semantics (the reference's plan coverage, combine.py:40-55 and
+// timemodel.py:78-96): part q of a plan covers count_q consecutive tau tiles
+// of size smem_q[tau] starting at sum_{p<q} count_p*smem_p[tau]; every other
+// space axis s is tiled uniformly by smem[s] from 0 with ceil(E_s/t_s) tiles
+// (the last one ragged; elements >= E_s are padding and never stored). Each
+// uKernel rectangle is then cut into MMA-sized work items (<= 128 lanes x 256
+// columns) — an implementation detail below the uKernel abstraction.
+#include <cuda.h>
+#include <cuda_runtime.h>
+#include <cudaTypedefs.h>
+
+#include <algorithm>
+#include <cstring>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "exec_types.h"
+#include "status.h"
+
+namespace ftb {
+
+cudaError_t launch_tc(const DevProblem*, const DevWork*, int32_t, int32_t, cudaStream_t);
+cudaError_t launch_ffma(const DevProblem*, const DevWork*, int32_t, int32_t, cudaStream_t);
+
+namespace {
+
+#define FTB_CUDA(call)                                                                     \
+  do {                                                                                     \
+    cudaError_t e_ = (call);                                                               \
+    if (e_ != cudaSuccess)                                                                 \
+      throw ::ftb::cuda_error(std::string(#call) + ": " + cudaGetErrorString(e_));                \
+  } while (0)
+
+PFN_cuTensorMapEncodeTiled_v12000 get_encode() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) ==
+            cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+  });
+  if (!fn) throw cuda_error("cuTensorMapEncodeTiled is unavailable (no CUDA driver?)");
+  return fn;
+}
+
+// 3-D bf16 tensor map: dims {inner, rows, batch}, SWIZZLE_128B, OOB = zeros.
+void encode_map(CUtensorMap* m, const void* base, int64_t inner, int64_t rows, int64_t batch,
+                int64_t ld_elems, int64_t batch_stride_elems, uint32_t box_inner,
+                uint32_t box_rows) {
+  if (reinterpret_cast<uintptr_t>(base) % 16)
+    throw input_error("tcgen05 path needs 16-byte aligned operand base pointers", "A/B");
+  if ((ld_elems * 2) % 16)
+    throw input_error("tcgen05 path needs row strides that are multiples of 8 bf16 elements",
+                      "ld");
+  cuuint64_t dims[3] = {static_cast<cuuint64_t>(inner), static_cast<cuuint64_t>(rows),
+                        static_cast<cuuint64_t>(batch)};
+  int64_t bs = batch > 1 ? batch_stride_elems : rows * ld_elems;
+  if ((bs * 2) % 16) throw input_error("batch stride must be a multiple of 8 elements", "batch");
+  cuuint64_t strides[2] = {static_cast<cuuint64_t>(ld_elems * 2), static_cast<cuuint64_t>(bs * 2)};
+  cuuint32_t box[3] = {box_inner, box_rows, 1};
+  cuuint32_t estr[3] = {1, 1, 1};
+  CUresult r = get_encode()(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<void*>(base), dims,
+                            strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                            CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) throw cuda_error("cuTensorMapEncodeTiled failed: " + std::to_string(r));
+}
+
+struct Region {
+  int64_t lo[3], hi[3];  // per space axis (dense uses 2)
+};
+
+int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }
+int64_t round_up(int64_t a, int64_t b) { return ceil_div(a, b) * b; }
+
+// Validate a program against its problem and enumerate the uKernel rectangles.
+std::vector<Region> plan_regions(const ftb_gemm_desc& d, const ftb_program& g,
+                                 int64_t* covered_out) {
+  const int ns = d.op == FTB_OP_BMM ? 3 : 2;
+  if (g.n_space != ns || g.n_reduce != 1)
+    throw input_error("program axis counts do not match the operator", "program");
+  if (g.tau < 0 || g.tau >= ns) throw input_error("program tau axis out of range", "tau");
+  if (g.n_parts < 1 || g.n_parts > 2) throw input_error("program needs one or two parts", "parts");
+  int64_t ext[3];
+  if (ns == 3) {
+    ext[0] = d.batch; ext[1] = d.M; ext[2] = d.N;
+  } else {
+    ext[0] = d.M; ext[1] = d.N;
+  }
+  for (int p = 0; p < g.n_parts; ++p) {
+    for (int a = 0; a < ns + 1; ++a)
+      if (g.smem[p][a] < 1) throw input_error("program tiles must be positive", "smem_tile");
+    for (int a = 0; a < ns; ++a)
+      if (g.reg[p][a] < 1 || g.smem[p][a] % g.reg[p][a])
+        throw input_error("register tile does not divide shared-memory tile", "reg_tile");
+    if (g.count[p] < 1) throw input_error("part counts must be >= 1", "count");
+  }
+  if (g.n_parts == 2)
+    for (int a = 0; a < ns + 1; ++a)
+      if (a != g.tau && g.smem[0][a] != g.smem[1][a])
+        throw input_error("parts disagree on a non-tau tile (combine.py:118-123)", "parts");
+  int64_t cover = 0;
+  for (int p = 0; p < g.n_parts; ++p) cover += g.count[p] * g.smem[p][g.tau];
+  if (cover != ext[g.tau])
+    throw input_error("program does not cover the main axis exactly (combine.py:189-193)", "tau");
+
+  std::vector<Region> out;
+  int64_t covered = 1;
+  for (int a = 0; a < ns; ++a)
+    if (a != g.tau) covered *= round_up(ext[a], g.smem[0][a]);
+  *covered_out = covered * ext[g.tau];
+
+  int64_t off = 0;
+  for (int p = 0; p < g.n_parts; ++p) {
+    const int64_t t = g.smem[p][g.tau];
+    for (int64_t c = 0; c < g.count[p]; ++c, off += t) {
+      // odometer over the non-tau axes
+      int64_t idx[3] = {0, 0, 0};
+      int64_t nt[3];
+      for (int a = 0; a < ns; ++a) nt[a] = (a == g.tau) ? 1 : ceil_div(ext[a], g.smem[p][a]);
+      while (true) {
+        Region r;
+        for (int a = 0; a < ns; ++a) {
+          if (a == g.tau) {
+            r.lo[a] = off;
+            r.hi[a] = off + t;
+          } else {
+            r.lo[a] = idx[a] * g.smem[p][a];
+            r.hi[a] = std::min(ext[a], r.lo[a] + g.smem[p][a]);
+          }
+        }
+        out.push_back(r);
+        int a = ns - 1;
+        for (; a >= 0; --a) {
+          if (++idx[a] < nt[a]) break;
+          idx[a] = 0;
+        }
+        if (a < 0) break;
+      }
+    }
+  }
+  return out;
+}
+
+struct Piece {
+  int64_t start, len;
+};
+void split(int64_t lo, int64_t hi, int64_t maxlen, std::vector<Piece>& out) {
+  out.clear();
+  const int64_t len = hi - lo;
+  const int64_t n = ceil_div(len, maxlen);
+  const int64_t base = ceil_div(len, n);
+  for (int64_t s = lo; s < hi; s += base) out.push_back({s, std::min(base, hi - s)});
+}
+
+}  // namespace
+
+struct ExecImpl {
+  std::vector<DevProblem> problems;
+  std::vector<DevWork> work;
+  DevProblem* d_problems = nullptr;
+  DevWork* d_work = nullptr;
+  ftb_exec_info info{};
+  ~ExecImpl() {
+    if (d_problems) cudaFree(d_problems);
+    if (d_work) cudaFree(d_work);
+  }
+};
+
+static int device_sms() {
+  int dev = 0, n = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) return 0;
+  if (cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess) return 0;
+  return n;
+}
+
+static void build(ExecImpl& ex, const ftb_gemm_desc* probs, const ftb_program* progs, int32_t n,
+                  bool encode) {
+  if (n < 1) throw input_error("no problems given", "problems");
+  const int32_t in_dt = probs[0].in_dtype;
+  for (int32_t p = 0; p < n; ++p)
+    if (probs[p].in_dtype != in_dt)
+      throw input_error("all problems of one table must share the input dtype", "in_dtype");
+  const bool ffma = in_dt == FTB_DT_F32;
+  ex.info.kernel = ffma ? 1 : 0;
+  std::vector<Piece> lp, cp;
+  struct Keyed {
+    int64_t cost;
+    DevWork w;
+  };
+  std::vector<Keyed> items;
+  for (int32_t p = 0; p < n; ++p) {
+    const ftb_gemm_desc& d = probs[p];
+    if (d.M < 1 || d.N < 1 || d.K < 1 || d.batch < 1)
+      throw input_error("problem extents must be >= 1", "shape");
+    if (d.op == FTB_OP_DENSE && d.batch != 1) throw input_error("dense problems have batch 1", "batch");
+    int64_t covered = 0;
+    std::vector<Region> regs = plan_regions(d, progs[p], &covered);
+    const int ib = d.op == FTB_OP_BMM ? 1 : 0;  // index of i among space axes
+    DevProblem P;
+    std::memset(&P, 0, sizeof(P));
+    P.A = d.A; P.B = d.B; P.C = d.C;
+    P.lda = d.lda; P.ldb = d.ldb; P.ldc = d.ldc;
+    P.a_bs = d.a_batch_stride; P.b_bs = d.b_batch_stride; P.c_bs = d.c_batch_stride;
+    P.M = static_cast<int32_t>(d.M); P.N = static_cast<int32_t>(d.N);
+    P.K = static_cast<int32_t>(d.K); P.batch = d.batch;
+    P.out_f32 = d.out_dtype == FTB_DT_F32;
+    P.b_nk = d.b_layout == FTB_B_NK;
+    P.num_kb = static_cast<int32_t>(ceil_div(d.K, kBlockK));
+    if (ffma && !P.out_f32) throw input_error("FFMA mode writes fp32 outputs", "out_dtype");
+
+    // Orientation: fewest tensor-core MMA cells (lanes padded to 128, columns
+    // to 16 or 64), ties to the normal orientation.
+    int swap = 0;
+    if (!ffma) {
+      int64_t cost[2] = {0, 0};
+      for (int o = 0; o < 2; ++o) {
+        const bool col_mn = (o == 0) && !P.b_nk;
+        const int64_t gran = col_mn ? 64 : 16;
+        for (const Region& r : regs) {
+          const int64_t li = r.hi[ib] - r.lo[ib], lj = r.hi[ib + 1] - r.lo[ib + 1];
+          const int64_t lane = o ? lj : li, col = o ? li : lj;
+          split(0, col, kMaxN, cp);
+          int64_t cols = 0;
+          for (auto& c : cp) cols += round_up(c.len, gran);
+          cost[o] += ceil_div(lane, kLaneRows) * kLaneRows * cols;
+        }
+      }
+      swap = d.orientation >= 0 ? d.orientation : (cost[1] < cost[0] ? 1 : 0);
+    }
+    P.swap = swap;
+    P.lane_mn = swap && !P.b_nk;
+    P.col_mn = !swap && !P.b_nk;
+    if (!ffma && d.in_dtype != FTB_DT_BF16) throw input_error("unsupported input dtype", "in_dtype");
+    if (!ffma && encode) {
+      // A: [batch][M][lda], K contiguous. B: [batch][N][ldb] (NK) or [batch][K][ldb] (KN).
+      if (!swap) {
+        encode_map(&P.tm_lane, d.A, d.K, d.M, d.batch, d.lda, d.a_batch_stride, 64, kLaneRows);
+        if (P.b_nk)
+          encode_map(&P.tm_col, d.B, d.K, d.N, d.batch, d.ldb, d.b_batch_stride, 64, kColBoxRows);
+        else
+          encode_map(&P.tm_col, d.B, d.N, d.K, d.batch, d.ldb, d.b_batch_stride, 64, 64);
+      } else {
+        if (P.b_nk)
+          encode_map(&P.tm_lane, d.B, d.K, d.N, d.batch, d.ldb, d.b_batch_stride, 64, kLaneRows);
+        else
+          encode_map(&P.tm_lane, d.B, d.N, d.K, d.batch, d.ldb, d.b_batch_stride, 64, 64);
+        encode_map(&P.tm_col, d.A, d.K, d.M, d.batch, d.lda, d.a_batch_stride, 64, kColBoxRows);
+      }
+    }
+    ex.problems.push_back(P);
+
+    const int64_t lane_max = ffma ? 64 : kLaneRows;
+    const int64_t col_max = ffma ? 64 : kMaxN;
+    const int64_t gran = P.col_mn ? 64 : 16;
+    for (const Region& r : regs) {
+      const int64_t b0 = ib ? r.lo[0] : 0, b1 = ib ? r.hi[0] : 1;
+      const int64_t ilo = r.lo[ib], ihi = r.hi[ib], jlo = r.lo[ib + 1], jhi = r.hi[ib + 1];
+      if (swap) {
+        split(jlo, jhi, lane_max, lp);
+        split(ilo, ihi, col_max, cp);
+      } else {
+        split(ilo, ihi, lane_max, lp);
+        split(jlo, jhi, col_max, cp);
+      }
+      for (int64_t b = b0; b < b1; ++b)
+        for (auto& L : lp)
+          for (auto& Cc : cp) {
+            DevWork w;
+            w.problem = p;
+            w.batch = static_cast<int32_t>(b);
+            w.lane0 = static_cast<int32_t>(L.start);
+            w.col0 = static_cast<int32_t>(Cc.start);
+            w.lane_len = static_cast<int32_t>(L.len);
+            w.col_len = static_cast<int32_t>(Cc.len);
+            w.n_mma = ffma ? static_cast<int32_t>(Cc.len) : static_cast<int32_t>(round_up(Cc.len, gran));
+            w.aux = 0;
+            const int64_t cost = static_cast<int64_t>(P.num_kb) * (ffma ? L.len : kLaneRows) * w.n_mma;
+            items.push_back({cost, w});
+            ex.info.mma_flops += 2 * cost * kBlockK;
+          }
+    }
+    ex.info.true_flops += 2 * d.batch * d.M * d.N * d.K;
+    ex.info.covered_out += covered;
+    ex.info.true_out += d.batch * d.M * d.N;
+  }
+  // Longest-first order so the static round-robin over persistent CTAs balances.
+  std::stable_sort(items.begin(), items.end(),
+                   [](const Keyed& a, const Keyed& b) { return a.cost > b.cost; });
+  ex.work.reserve(items.size());
+  for (auto& k : items) ex.work.push_back(k.w);
+  ex.info.n_work = static_cast<int64_t>(ex.work.size());
+  ex.info.n_problems = n;
+  int sms = device_sms();
+  if (sms <= 0) sms = 148;
+  ex.info.n_ctas = std::min<int64_t>(ex.info.n_work, ffma ? 4 * sms : sms);
+  if (ex.info.n_work > INT32_MAX) throw input_error("tile table too large", "work");
+}
+
+}  // namespace ftb
+
+struct ftb_exec {
+  ftb::ExecImpl impl;
+};
+
+extern "C" {
+
+int32_t ftb_device_sm_count(void) { return ftb::device_sms(); }
+
+ftb_status ftb_exec_create(const ftb_gemm_desc* problems, const ftb_program* programs, int32_t n,
+                           ftb_exec** out) {
+  return ftb::guarded([&] {
+    if (!out || !problems || !programs) throw ftb::input_error("null argument");
+    auto* ex = new ftb_exec();
+    try {
+      ftb::build(ex->impl, problems, programs, n, /*encode=*/true);
+      auto& I = ex->impl;
+      FTB_CUDA(cudaMalloc(&I.d_problems, sizeof(ftb::DevProblem) * I.problems.size()));
+      FTB_CUDA(cudaMemcpy(I.d_problems, I.problems.data(),
+                          sizeof(ftb::DevProblem) * I.problems.size(), cudaMemcpyHostToDevice));
+      if (!I.work.empty()) {
+        FTB_CUDA(cudaMalloc(&I.d_work, sizeof(ftb::DevWork) * I.work.size()));
+        FTB_CUDA(cudaMemcpy(I.d_work, I.work.data(), sizeof(ftb::DevWork) * I.work.size(),
+                            cudaMemcpyHostToDevice));
+      }
+    } catch (...) {
+      delete ex;
+      throw;
+    }
+    *out = ex;
+  });
+}
+
+ftb_status ftb_exec_launch(ftb_exec* ex, void* stream) {
+  return ftb::guarded([&] {
+    if (!ex) throw ftb::input_error("null exec");
+    auto& I = ex->impl;
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    cudaError_t e = I.info.kernel == 1
+                        ? ftb::launch_ffma(I.d_problems, I.d_work, static_cast<int32_t>(I.info.n_work),
+                                           static_cast<int32_t>(I.info.n_ctas), s)
+                        : ftb::launch_tc(I.d_problems, I.d_work, static_cast<int32_t>(I.info.n_work),
+                                         static_cast<int32_t>(I.info.n_ctas), s);
+    if (e != cudaSuccess) throw ftb::cuda_error(std::string("kernel launch: ") + cudaGetErrorString(e));
+  });
+}
+
+ftb_status ftb_exec_get_info(const ftb_exec* ex, ftb_exec_info* info) {
+  return ftb::guarded([&] {
+    if (!ex || !info) throw ftb::input_error("null argument");
+    *info = ex->impl.info;
+  });
+}
+
+ftb_status ftb_exec_export_table(const ftb_exec* ex, int32_t* out, int64_t cap, int64_t* n_out) {
+  return ftb::guarded([&] {
+    if (!ex || !n_out) throw ftb::input_error("null argument");
+    const auto& W = ex->impl.work;
+    *n_out = static_cast<int64_t>(W.size());
+    if (out) {
+      const int64_t k = std::min<int64_t>(cap, static_cast<int64_t>(W.size()));
+      std::memcpy(out, W.data(), sizeof(ftb::DevWork) * k);
+    }
+  });
+}
+
+void ftb_exec_destroy(ftb_exec* ex) { delete ex; }
+
+ftb_status ftb_lower(const ftb_gemm_desc* problems, const ftb_program* programs, int32_t n,
+                     int32_t* out, int64_t cap, int64_t* n_out, ftb_exec_info* info) {
+  return ftb::guarded([&] {
+    if (!problems || !programs || !n_out) throw ftb::input_error("null argument");
+    ftb::ExecImpl I;
+    ftb::build(I, problems, programs, n, /*encode=*/false);
+    *n_out = static_cast<int64_t>(I.work.size());
+    if (out) {
+      const int64_t k = std::min<int64_t>(cap, static_cast<int64_t>(I.work.size()));
+      std::memcpy(out, I.work.data(), sizeof(ftb::DevWork) * k);
+    }
+    if (info) *info = I.info;
+  });
+}
+
+}  // extern "C"

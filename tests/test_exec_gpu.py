@@ -1,0 +1,128 @@
+"""Executor numerics on B200: hand-built plans of every shape class vs a
+plain fp32 reference of the same op (norm-wise relative error)."""
+
+import pytest
+import torch
+
+from paper_2407_21418_b200.execute import Executable, gemm_desc, program_struct
+
+pytestmark = pytest.mark.gpu
+
+BF16_TOL = 2e-2
+F32_TOL = 1e-5
+
+
+def _rel(c, ref):
+    return ((c.float() - ref).abs().max() / ref.abs().max().clamp_min(1e-30)).item()
+
+
+def _dense(M, N, K, b_layout, dtype, dev, seed=0):
+    g = torch.Generator(device="cpu").manual_seed(seed)
+    A = (torch.rand(M, K, generator=g) * 2 - 1).to(dtype).to(dev)
+    Bkn = (torch.rand(K, N, generator=g) * 2 - 1).to(dtype).to(dev)
+    B = Bkn if b_layout == "kn" else Bkn.t().contiguous()
+    ref = A.double() @ Bkn.double()
+    return A, B, ref
+
+
+DENSE_CASES = [
+    # (M, N, K, tau, parts[(reg, smem, count)])
+    (256, 512, 256, 1, [((1, 8), (128, 128, 64), 4)]),
+    (200, 320, 200, 1, [((1, 8), (30, 64, 64), 3), ((1, 8), (30, 128, 64), 1)]),
+    (5, 768, 768, 1, [((1, 8), (8, 64, 64), 12)]),
+    (1, 768, 768, 1, [((1, 1), (1, 64, 64), 12)]),
+    (509, 768, 768, 1, [((1, 8), (30, 32 * 2, 64), 12)]),
+    (4096, 1024, 512, 0, [((1, 8), (128, 256, 64), 32)]),
+    (1696, 2304, 768, 1, [((1, 8), (106, 128, 64), 18)]),
+    (300, 256, 72, 0, [((2, 8), (100, 256, 64), 3)]),
+]
+
+
+@pytest.mark.parametrize("case", DENSE_CASES, ids=lambda c: f"M{c[0]}N{c[1]}K{c[2]}")
+@pytest.mark.parametrize("b_layout", ["kn", "nk"])
+@pytest.mark.parametrize("orientation", [-1, 0, 1])
+def test_dense_bf16(cuda, case, b_layout, orientation):
+    M, N, K, tau, parts = case
+    A, B, ref = _dense(M, N, K, b_layout, torch.bfloat16, cuda)
+    Cout = torch.empty(M, N, dtype=torch.bfloat16, device=cuda)
+    Cout.fill_(float("nan"))
+    ex = Executable([gemm_desc(A, B, Cout, b_layout, orientation)], [program_struct(2, tau, parts)])
+    ex.launch()
+    torch.cuda.synchronize()
+    assert not torch.isnan(Cout.float()).any(), "uncovered output elements"
+    assert _rel(Cout, ref) < BF16_TOL
+
+
+@pytest.mark.parametrize("b_layout", ["kn", "nk"])
+def test_dense_f32_out(cuda, b_layout):
+    M, N, K = 130, 384, 192
+    A, B, ref = _dense(M, N, K, b_layout, torch.bfloat16, cuda, seed=3)
+    Cout = torch.full((M, N), float("nan"), dtype=torch.float32, device=cuda)
+    ex = Executable([gemm_desc(A, B, Cout, b_layout)], [program_struct(2, 1, [((1, 8), (65, 128, 64), 3)])])
+    ex.launch()
+    torch.cuda.synchronize()
+    assert _rel(Cout, ref) < 1e-2
+
+
+@pytest.mark.parametrize("T", [1, 5, 37, 64, 128])
+@pytest.mark.parametrize("kind", ["scores", "context"])
+def test_bmm_bf16(cuda, T, kind):
+    b = 6
+    g = torch.Generator().manual_seed(T)
+    if kind == "scores":
+        # Q [b,T,64] @ K^T: B given as K [b, T(j), 64(k)] -> "nk" layout
+        M, N, Kd, layout = T, T, 64, "nk"
+    else:
+        # P [b,T,T] @ V [b,T(k),64(j)] -> "kn" layout; P row stride padded to 8
+        M, N, Kd, layout = T, 64, T, "kn"
+    ldk = (Kd + 7) // 8 * 8
+    Abuf = torch.zeros(b, M, ldk, dtype=torch.bfloat16)
+    Abuf[:, :, :Kd] = (torch.rand(b, M, Kd, generator=g) * 2 - 1).to(torch.bfloat16)
+    A = Abuf.to(cuda)[:, :, :Kd]
+    if layout == "nk":
+        Bt = (torch.rand(b, N, Kd, generator=g) * 2 - 1).to(torch.bfloat16).to(cuda)
+        Bkn = Bt.transpose(1, 2)
+        B = Bt
+    else:
+        B = (torch.rand(b, Kd, N, generator=g) * 2 - 1).to(torch.bfloat16).to(cuda)
+        Bkn = B
+    ref = A.double() @ Bkn.double()
+    Cout = torch.full((b, M, N), float("nan"), dtype=torch.bfloat16, device=cuda)
+    jt = ((N + 63) // 64) * 64
+    parts = [((1, 1, 1), (1, M, jt, 64), b)]  # tau = b, one batch entry per uKernel
+    ex = Executable([gemm_desc(A, B, Cout, layout)], [program_struct(3, 0, parts)])
+    ex.launch()
+    torch.cuda.synchronize()
+    assert not torch.isnan(Cout.float()).any()
+    assert _rel(Cout, ref) < BF16_TOL
+
+
+def test_grouped_launch(cuda):
+    """Many problems of different shapes and plans in ONE launch."""
+    descs, progs, refs, outs, keep = [], [], [], [], []
+    for s, (M, N, K, tau, parts) in enumerate(DENSE_CASES[:6]):
+        A, B, ref = _dense(M, N, K, "nk", torch.bfloat16, cuda, seed=10 + s)
+        Cout = torch.full((M, N), float("nan"), dtype=torch.bfloat16, device=cuda)
+        descs.append(gemm_desc(A, B, Cout, "nk"))
+        progs.append(program_struct(2, tau, parts))
+        refs.append(ref)
+        outs.append(Cout)
+        keep += [A, B, Cout]
+    ex = Executable(descs, progs, keep)
+    ex.launch()
+    torch.cuda.synchronize()
+    for c, r in zip(outs, refs):
+        assert _rel(c, r) < BF16_TOL
+
+
+@pytest.mark.parametrize("M", [1, 53, 509])
+@pytest.mark.parametrize("b_layout", ["kn", "nk"])
+def test_dense_ffma_fp32(cuda, M, b_layout):
+    N = K = 768
+    A, B, ref = _dense(M, N, K, b_layout, torch.float32, cuda, seed=M)
+    Cout = torch.full((M, N), float("nan"), dtype=torch.float32, device=cuda)
+    ex = Executable([gemm_desc(A, B, Cout, b_layout)], [program_struct(2, 1, [((1, 8), (30, 64, 32), 12)])])
+    ex.launch()
+    torch.cuda.synchronize()
+    assert ex.info.kernel == "ffma"
+    assert _rel(Cout, ref) < F32_TOL
