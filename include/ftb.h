@@ -67,6 +67,102 @@ typedef struct {
 } ftb_program;
 
 /* ------------------------------------------------------------------------ */
+/* Planner (enumerate -> annotate -> filter -> relax -> compose -> rank)     */
+/* ------------------------------------------------------------------------ */
+
+/* HardwareDescriptor (hardware.py:35-66): the 9 integer fields, plus the
+ * B200 legality extension (0 = parity mode, exactly the reference). */
+typedef struct {
+  int64_t num_cores, regs_per_core, smem_per_core_bytes;
+  int64_t global_bw_bytes_per_s, shared_bw_bytes_per_s, peak_flops;
+  int64_t default_active_blocks, active_blocks_per_core, align_elems;
+  int32_t legality;   /* 0 = parity (reference), 1 = tcgen05 tile legality */
+  int32_t reserved;
+} ftb_hw;
+
+/* A bound WorkloadInstance (workload.py:187-220) flattened. Axis indices
+ * run over the spec's space axes then its reduce axes (axis_names order of
+ * ukernel.py:250-252). */
+#define FTB_MAX_INPUTS 4
+typedef struct {
+  int32_t n_space, n_reduce;
+  int32_t major;                                  /* space index of the major axis (ukernel.py:93-95) */
+  int32_t n_inputs;
+  int32_t input_naxes[FTB_MAX_INPUTS];
+  int32_t input_axes[FTB_MAX_INPUTS][FTB_MAX_AXES];
+  int32_t elem_bytes, flops_per_point;
+  int64_t extent[FTB_MAX_AXES];
+  int32_t dynamic[FTB_MAX_AXES];
+  char axis_name[FTB_MAX_AXES][16];
+} ftb_instance;
+
+typedef struct { int64_t num, den; } ftb_frac;
+
+/* FilterParams + SweepParams (filtering.py:77-128, :237-250). */
+typedef struct {
+  ftb_frac eps_min, eps_max, lam_min, lam_max, eps_step, lam_step;
+  double psi;
+  int64_t rest_regs;
+  int64_t candidate_cap;   /* < 0 = no cap (None) */
+} ftb_params;
+
+typedef struct { double c0, c1, c2; } ftb_coeffs;   /* SiaCoeffs (scoring.py:23-38) */
+
+enum { FTB_RELAX_NONE = 0, FTB_RELAX_DROP_INTENSITY = 1, FTB_RELAX_DROP_SATURATION = 2,
+       FTB_RELAX_WIDEN = 3, FTB_RELAX_DROP_SWEEP = 4 };
+
+/* ShapeResult provenance (filtering.py:253-264, :334-348). */
+typedef struct {
+  int64_t n_align, n_cross, n_filter, n_final;
+  int32_t relaxation;      /* FTB_RELAX_*                                 */
+  int32_t widen;           /* N of "widen-sweep-N"                        */
+  int32_t truncated;
+  int32_t tau;             /* select_main_axis (combine.py:58-68)         */
+  ftb_frac sweep_used[6];  /* eps_min, eps_max, lam_min, lam_max, eps_step, lam_step */
+  double seconds;
+} ftb_compile_report;
+
+/* Columnar candidate set (CandidateSet, ukernel.py:219-313) owned by the library. */
+typedef struct ftb_cands ftb_cands;
+
+/* enumerate_ukernels (ukernel.py:341-437): canonical order, cap truncation. */
+ftb_status ftb_enumerate(const ftb_hw* hw, const ftb_instance* inst, int64_t cap,
+                         ftb_cands** out, int32_t* truncated);
+/* compile_shape (filtering.py:270-348): the final set with cached metrics. */
+ftb_status ftb_compile_shape(const ftb_hw* hw, const ftb_instance* inst, const ftb_params* p,
+                             ftb_cands** out, ftb_compile_report* rep);
+/* A candidate table from caller arrays (build_programs on arbitrary UKernels,
+ * combine.py:133). Metric pointers may be NULL; NaN = metric not cached. */
+ftb_status ftb_cands_from_arrays(const ftb_instance* inst, int64_t n, const int64_t* reg,
+                                 const int64_t* smem, const double* pad, const double* occ,
+                                 const double* cmr, ftb_cands** out);
+int64_t ftb_cands_size(const ftb_cands* c);
+/* Row-major exports: reg[n][n_space], smem[n][n_space+n_reduce];
+ * icol[n][7] = pad_num, pad_den, blocks, occ_den, regs_in_block, saturated,
+ * retained_step; fcol[n][2] = cmr, kmem. Any pointer may be NULL. */
+ftb_status ftb_cands_export(const ftb_cands* c, int64_t* reg, int64_t* smem, int64_t* icol,
+                            double* fcol);
+void ftb_cands_destroy(ftb_cands* c);
+
+/* select_main_axis (combine.py:58-68). */
+ftb_status ftb_select_main_axis(const ftb_instance* inst, int32_t* tau);
+/* Size of the program pool build_programs would materialise (combine.py:133-194). */
+ftb_status ftb_pool_count(const ftb_cands* c, int32_t tau, int64_t* n);
+/* The pool in canonical plan-key order (combine.py:182): rows[i] =
+ * {nparts, row_a, count_a, row_b, count_b} with rows into the candidate table. */
+ftb_status ftb_pool_export(const ftb_cands* c, int32_t tau, int64_t cap, int64_t* rows,
+                           int64_t* n);
+/* rank_programs (scoring.py:83-126) over the implicit pool, streamed: the
+ * pool is never materialised. rows as ftb_pool_export, scores[i] = sia. */
+ftb_status ftb_rank_topk(const ftb_cands* c, int32_t tau, const ftb_coeffs* coeffs, int32_t k,
+                         int32_t normalize, int64_t* rows, double* scores, int32_t* n_out);
+/* compile_stage (filtering.py:376-405) + build/rank Top-1 for many shapes on
+ * a host thread pool; out[i] is the Top-1 program of inst[i]. */
+ftb_status ftb_plan_batch(const ftb_hw* hw, const ftb_instance* insts, int32_t n,
+                          const ftb_params* p, const ftb_coeffs* coeffs, int32_t threads,
+                          ftb_program* out, ftb_compile_report* reps, ftb_status* statuses);
+
+/* ------------------------------------------------------------------------ */
 /* Execution (the reference has none: SPEC.md:8 — this is the new L6)       */
 /* ------------------------------------------------------------------------ */
 
