@@ -1,0 +1,414 @@
+#!/usr/bin/env python3
+"""Benchmark: dynamic-shape Dense+BMM over the C1 shape set (BERT-base,
+batch 32, GLUE-like sequence lengths), executed as mixed-size uKernels by one
+persistent sm_100a launch per step.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+One process per GPU (torchrun for N>1). Each rank draws its own sequence
+lengths (seed = rank), so per-GPU work is fixed as N grows ("weak"); there is
+no collective on the data path — ranks only meet at the timing barriers and
+the final max-over-ranks reduction. Rank 0 prints ONE JSON line.
+
+A "step" = one pass of the hot path over the whole shape set: every Dense
+and BMM of every sequence length, executed from the lowered tile table.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+from pathlib import Path
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+METRIC = "dynamic-shape GEMM TFLOP/s (shape-set mean) vs roofline; tuning s; padding %"
+WORKLOAD = "C1: BERT-base encoder Dense+BatchMatmul, batch 32, GLUE-like seq lengths 5-128 (8 canonical T + 24 drawn), bf16"
+
+
+def measured_peaks() -> dict:
+    p = ROOT / "MEASURED_PEAKS.json"
+    if p.exists():
+        d = json.loads(p.read_text())
+        return {"hbm_gbs": d["hbm_gbs"], "bf16_tflops": d["bf16_tflops"],
+                "bf16_tflops_sustained": d.get("bf16_tflops_sustained"), "source": "measured"}
+    return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0, "source": "fallback"}
+
+
+# ----------------------------------------------------------------------------- clocks
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled every 100 ms."""
+
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.rows: list[list[str]] = []
+        self.proc = None
+        self.thread = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
+                 "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except (OSError, FileNotFoundError):
+            self.proc = None
+            return self
+
+        def read():
+            for line in self.proc.stdout:
+                self.rows.append([c.strip() for c in line.split(",")])
+
+        self.thread = threading.Thread(target=read, daemon=True)
+        self.thread.start()
+        return self
+
+    def stop(self) -> dict:
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"], "samples": 0}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=2)
+        except subprocess.TimeoutExpired:
+            self.proc.kill()
+        if self.thread:
+            self.thread.join(timeout=2)
+        sm, smax, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for r in self.rows:
+            try:
+                sm.append(float(r[1]))
+                smax.append(float(r[2]))
+                for n, v in zip(names, r[4:8]):
+                    if v.lower().startswith("active"):
+                        reasons.add(n)
+            except (ValueError, IndexError):
+                continue
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(smax) if smax else None,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# ----------------------------------------------------------------------------- distributed
+
+
+def dist_init():
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world > 1:
+        import torch
+        import torch.distributed as dist
+
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    return rank, world, local
+
+
+def barrier(world):
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.barrier()
+
+
+def max_over_ranks(x: float, world: int) -> float:
+    if world == 1:
+        return x
+    import torch
+    import torch.distributed as dist
+
+    t = torch.tensor([x], dtype=torch.float64, device="cuda")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def sum_over_ranks(x: float, world: int) -> float:
+    if world == 1:
+        return x
+    import torch
+    import torch.distributed as dist
+
+    t = torch.tensor([x], dtype=torch.float64, device="cuda")
+    dist.all_reduce(t, op=dist.ReduceOp.SUM)
+    return float(t.item())
+
+
+# ----------------------------------------------------------------------------- cpu baseline
+
+
+def cpu_execute_sample(shapes, seconds_budget: float = 20.0) -> dict:
+    """ORACLE leg (bench.py cpu_baseline / --impl reference only): the numpy
+    fp32 restatement of plan execution (oracle/execute_np.py) over the shape
+    set, on all host cores; bounded to ~seconds_budget."""
+    import numpy as np
+
+    from oracle.execute_np import execute_dense_fp32
+
+    rng = np.random.default_rng(0)
+    flops = 0
+    t_total = 0.0
+    done = 0
+    t_start = time.perf_counter()
+    for s in shapes:
+        A = rng.uniform(-1, 1, (s.batch, s.M, s.K)).astype(np.float32)
+        B = rng.uniform(-1, 1, (s.batch if s.kind == "bmm" else 1, s.K, s.N)).astype(np.float32)
+        t0 = time.perf_counter()
+        execute_dense_fp32(A, B)
+        t_total += time.perf_counter() - t0
+        flops += s.flops
+        done += 1
+        if time.perf_counter() - t_start > seconds_budget:
+            break
+    return {"tflops": flops / t_total / 1e12, "shapes": done, "seconds": t_total}
+
+
+# ----------------------------------------------------------------------------- arms
+
+
+def run_reference(args, rank, world):
+    """--impl reference: the reference's CPU path restated by the oracle
+    (numpy fp32 execute of the same shape set) on the host cores."""
+    if rank != 0:
+        return
+    from paper_2407_21418_b200.workloads import c1_shapes
+
+    shapes = c1_shapes(n_draws=args.draws, seed=0)
+    sample = [s for s in shapes][: 6 * 8]  # the 8 canonical sequence lengths (48 GEMMs)
+    cores = os.cpu_count()
+    for _ in range(args.warmup):
+        cpu_execute_sample(sample[:6], 5.0)
+    vals = []
+    t_all = time.perf_counter()
+    for _ in range(args.steps):
+        vals.append(cpu_execute_sample(sample, 60.0))
+    wall = time.perf_counter() - t_all
+    flops = sum(v["tflops"] * v["seconds"] * 1e12 for v in vals)
+    secs = sum(v["seconds"] for v in vals)
+    value = flops / secs / 1e12
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": "TFLOP/s", "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * secs / max(1, args.steps),
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+        "config": {"workload": WORKLOAD, "sample": "8 canonical T x 6 GEMMs (48 shapes) per step",
+                   "parallelism": "cpu"},
+        "cpu_baseline": {"value": value, "unit": "TFLOP/s", "cores": cores, "kind": "port",
+                         "sample": "numpy fp32 A@B (OpenBLAS, all cores) over 48 C1 GEMMs per step"},
+        "e2e": {"value": value, "unit": "TFLOP/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "wall_s": wall,
+    }
+    print(json.dumps(line), flush=True)
+
+
+def load_traffic(tag: str):
+    p = ROOT / "profiles" / "ncu_traffic.json"
+    if not p.exists():
+        return None
+    try:
+        d = json.loads(p.read_text())
+        return d.get(tag)
+    except json.JSONDecodeError:
+        return None
+
+
+def run_ours(args, rank, world, local):
+    import torch
+
+    from paper_2407_21418_b200.runtime import Planner
+    from paper_2407_21418_b200.shapeset import ShapeSet
+    from paper_2407_21418_b200.workloads import c1_shapes
+
+    dev = torch.device("cuda", local)
+    torch.cuda.set_device(dev)
+    peaks = measured_peaks()
+    P = peaks["bf16_tflops"] * 1e12
+    shapes = c1_shapes(n_draws=args.draws, seed=rank)
+    if args.ops != "all":
+        shapes = [s for s in shapes if s.kind == args.ops]
+    planner = Planner()
+    ss = ShapeSet(shapes, planner, device=dev, seed=rank, pinned=True)
+    stream = torch.cuda.current_stream(dev)
+    info = ss.exe.info
+
+    # ------------------------------------------------ device-resident timing
+    clocks = ClockSampler(local).start()
+    t_end = time.perf_counter() + args.min_warm_s
+    w = 0
+    while w < args.warmup or time.perf_counter() < t_end:
+        ss.launch(stream)
+        w += 1
+        if w % 50 == 0:
+            torch.cuda.synchronize(dev)
+    torch.cuda.synchronize(dev)
+    barrier(world)
+    torch.cuda.synchronize(dev)
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    for e0, e1 in ev:
+        e0.record(stream)
+        ss.launch(stream)
+        e1.record(stream)
+    torch.cuda.synchronize(dev)
+    barrier(world)
+    per_launch = [e0.elapsed_time(e1) for e0, e1 in ev]  # ms, on the launching stream
+    clk = clocks.stop()
+    t_step_ms = sum(per_launch) / len(per_launch)
+    t_max_ms = max_over_ranks(t_step_ms, world)
+
+    # ------------------------------------------------ end-to-end (host buffers)
+    for _ in range(2):
+        ss.step_e2e(stream)
+    torch.cuda.synchronize(dev)
+    barrier(world)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e2e_steps = max(1, min(args.steps, 10))
+    e0.record(stream)
+    for _ in range(e2e_steps):
+        ss.step_e2e(stream)
+    e1.record(stream)
+    torch.cuda.synchronize(dev)
+    e2e_ms = max_over_ranks(e0.elapsed_time(e1) / e2e_steps, world)
+
+    # ------------------------------------------------ per-shape roofline fractions
+    # (one launch per shape, back to back in a CUDA graph; shape-set mean)
+    shape_fracs = None
+    if args.per_shape and world == 1:
+        shape_fracs = per_shape_fracs(ss, planner, P, dev)
+
+    flops_rank = ss.true_flops
+    flops_all = sum_over_ranks(float(flops_rank), world)
+    bytes_rank = ss.alg_bytes
+    value = flops_all / (t_max_ms * 1e-3) / 1e12
+    e2e_value = flops_all / (e2e_ms * 1e-3) / 1e12
+    t_roof_sum = sum(s.t_roof(P) for s in ss.shapes)
+    # dominant kernel = the single persistent launch of the step
+    t_tc = flops_rank / P
+    t_hbm = bytes_rank / (peaks["hbm_gbs"] * 1e9)
+    bound = "tensor" if t_tc >= t_hbm else "hbm"
+    if bound == "tensor":
+        achieved = flops_rank / (t_step_ms * 1e-3) / 1e12
+        roof = {"bound": "tensor", "achieved": achieved, "peak": peaks["bf16_tflops"], "unit": "TFLOP/s",
+                "frac": achieved / peaks["bf16_tflops"]}
+    else:
+        achieved = bytes_rank / (t_step_ms * 1e-3) / 1e9
+        roof = {"bound": "hbm", "achieved": achieved, "peak": peaks["hbm_gbs"], "unit": "GB/s",
+                "frac": achieved / peaks["hbm_gbs"]}
+    roof["traffic"] = load_traffic("c1_step")
+    roof["peak_source"] = peaks["source"] + " (MEASURED_PEAKS.json burst)" if peaks["source"] == "measured" else "fallback"
+    roof["algorithmic_flops_per_launch"] = flops_rank
+    roof["algorithmic_bytes_per_launch"] = bytes_rank
+
+    line = {
+        "metric": METRIC, "value": value, "unit": "TFLOP/s", "n_gpus": world, "steps": args.steps,
+        "warmup": w, "ms_per_step": t_max_ms, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "dtype": "bf16", "data": "synthetic (U(-1,1) bf16 activations and weights, seeded per rank)",
+        "config": {
+            "workload": WORKLOAD, "n_shapes_per_gpu": len(shapes), "shapes_per_step": len(shapes),
+            "parallelism": f"shape-sharded x{world} (no data-path collective)",
+            "l2": f"no flush: step footprint {(ss.alg_bytes) / 1e9:.2f} GB > 126 MB L2",
+        },
+        "roofline": roof,
+        "roofline_sum_of_shapes": {"t_roof_ms": t_roof_sum * 1e3, "frac_of_step": t_roof_sum * 1e3 / t_step_ms},
+        "shape_set_mean_roofline_frac": None if shape_fracs is None else shape_fracs["mean_frac"],
+        "shape_set_mean_tflops": None if shape_fracs is None else shape_fracs["mean_tflops"],
+        "tuning_s": ss.tuning_s,
+        "tuning_s_per_shape": ss.tuning_s / len(shapes),
+        "padding_pct": 100.0 * ss.padding_ratio(),
+        "mma_padding_pct": 100.0 * (1 - info.true_flops / info.mma_flops) if info.mma_flops else None,
+        "e2e": {"value": e2e_value, "unit": "TFLOP/s", "h2d_bytes_per_step": ss.h2d_bytes,
+                "d2h_bytes_per_step": ss.d2h_bytes, "ms_per_step": e2e_ms},
+        "gpu_launches": args.steps,
+        "work_items": info.n_work, "ctas": info.n_ctas,
+        "clocks": clk,
+    }
+    if rank == 0 and world == 1 and not args.no_cpu:
+        cb = cpu_execute_sample([s for s in shapes][:48], 20.0)
+        line["cpu_baseline"] = {"value": cb["tflops"], "unit": "TFLOP/s", "cores": os.cpu_count(), "kind": "port",
+                                "sample": f"numpy fp32 A@B over {cb['shapes']} C1 GEMMs (8 canonical T), "
+                                          f"{cb['seconds']:.1f} s, OpenBLAS all cores"}
+    if shape_fracs is not None:
+        line["per_shape"] = shape_fracs["rows"] if args.per_shape_rows else None
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+
+
+def per_shape_fracs(ss, planner, P, dev):
+    """Each shape as its own launch (its own single-problem table), timed
+    back to back inside a CUDA graph; fraction = t_roof / t_measured."""
+    import torch
+
+    from paper_2407_21418_b200.execute import Executable, gemm_desc
+
+    rows = []
+    exes = []
+    for x, rec in zip(ss.bound, ss.records):
+        exes.append(Executable([gemm_desc(x.A, x.B, x.C, x.shape.b_layout)], [rec.program], (x.A, x.B, x.C)))
+    s = torch.cuda.Stream(dev)
+    reps = 20
+    with torch.cuda.stream(s):
+        for e in exes:
+            e.launch(s)
+    torch.cuda.synchronize(dev)
+    for e, x in zip(exes, ss.bound):
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g, stream=s):
+            for _ in range(reps):
+                e.launch(s)
+        with torch.cuda.stream(s):
+            g.replay()
+        torch.cuda.synchronize(dev)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        with torch.cuda.stream(s):
+            e0.record(s)
+            g.replay()
+            e1.record(s)
+        torch.cuda.synchronize(dev)
+        t = e0.elapsed_time(e1) / reps * 1e-3
+        sh = x.shape
+        rows.append({"name": sh.name, "b": sh.batch, "M": sh.M, "N": sh.N, "K": sh.K, "us": t * 1e6,
+                     "tflops": sh.flops / t / 1e12, "frac": sh.t_roof(P) / t, "bound": sh.bound(P)})
+    return {"rows": rows, "mean_frac": sum(r["frac"] for r in rows) / len(rows),
+            "mean_tflops": sum(r["tflops"] for r in rows) / len(rows)}
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=50)
+    ap.add_argument("--warmup", type=int, default=10)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--draws", type=int, default=24)
+    ap.add_argument("--min-warm-s", type=float, default=1.0)
+    ap.add_argument("--per-shape", type=int, default=1)
+    ap.add_argument("--per-shape-rows", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--ops", choices=["all", "dense", "bmm"], default="all")
+    args = ap.parse_args()
+    args.warmup = max(3, args.warmup)
+    if args.impl == "reference":
+        rank = int(os.environ.get("RANK", "0"))
+        world = int(os.environ.get("WORLD_SIZE", "1"))
+        run_reference(args, rank, world)
+        return
+    rank, world, local = dist_init()
+    try:
+        run_ours(args, rank, world, local)
+    finally:
+        if world > 1:
+            import torch.distributed as dist
+
+            dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

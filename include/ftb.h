@@ -119,6 +119,9 @@ typedef struct {
   int32_t truncated;
   int32_t tau;             /* select_main_axis (combine.py:58-68)         */
   ftb_frac sweep_used[6];  /* eps_min, eps_max, lam_min, lam_max, eps_step, lam_step */
+  int32_t stage;           /* set ranked by ftb_plan_batch: 0 final; B200-mode fallback
+                              rungs 1 filter, 2 cross, 3 align (extension)          */
+  int32_t reserved;
   double seconds;
 } ftb_compile_report;
 

@@ -29,6 +29,7 @@ static void fill_report(const Report& r, double secs, ftb_compile_report* out) {
   const Frac f[6] = {r.used.eps_min, r.used.eps_max, r.used.lam_min,
                      r.used.lam_max, r.used.eps_step, r.used.lam_step};
   for (int i = 0; i < 6; ++i) out->sweep_used[i] = {f[i].n, f[i].d};
+  out->stage = r.stage;
   out->seconds = secs;
 }
 
@@ -206,10 +207,21 @@ ftb_status ftb_plan_batch(const ftb_hw* hw, const ftb_instance* insts, int32_t n
         try {
           Instance in = Instance::from_c(insts[i]);
           Report r;
-          Cands c = compile_shape(in, h, q, &r);
-          auto top = rank_topk(c, r.tau, *coeffs, 1, false);
-          if (top.empty()) throw FtbError(FTB_EMPTY_RESULT, "empty program pool", "program pool");
-          fill_program(c, r.tau, top[0].first, top[0].second, &out[i]);
+          // Parity mode ranks the final set only (an empty pool raises, as
+          // combine.py:183-188 does). B200 mode falls back to the filter,
+          // cross and align sets when no final-set combination covers tau.
+          const int last = h.legality ? 3 : 0;
+          for (int stage = 0;; ++stage) {
+            Cands c = compile_shape(in, h, q, &r, stage);
+            try {
+              auto top = rank_topk(c, r.tau, *coeffs, 1, false);
+              if (top.empty()) throw FtbError(FTB_EMPTY_RESULT, "empty program pool", "program pool");
+              fill_program(c, r.tau, top[0].first, top[0].second, &out[i]);
+              break;
+            } catch (const FtbError& e) {
+              if (e.code != FTB_EMPTY_RESULT || stage >= last) throw;
+            }
+          }
           fill_report(r, secs_since(t0), reps ? &reps[i] : nullptr);
         } catch (const FtbError& e) {
           st[i] = e.code;

@@ -27,6 +27,7 @@ static inline int64_t py_floordiv(int64_t a, int64_t b) {
   return q;
 }
 static inline int64_t py_ceildiv(int64_t a, int64_t b) { return -py_floordiv(-a, b); }
+static constexpr int64_t _MAX_WIDEN = 2000;  // filtering.py:267
 
 Frac Frac::make(int64_t n, int64_t d) {
   if (d == 0) throw input_error("zero denominator in sweep parameter");
@@ -178,15 +179,18 @@ static std::vector<int64_t> reduce_options(int64_t e, int64_t align) {  // ukern
 }
 
 bool tcgen05_legal(const Instance& in, const int64_t* smem) {
-  // B200 extension: the uKernel's output tile must map onto tcgen05 tiles
-  // (M in {64,128,...,256} TMEM lanes x N multiple of 16 <= 256 columns) in
-  // one of the two orientations; a tile covering a whole short axis is
-  // also accepted. Batch tiles are free (one work item per batch entry).
+  // B200 extension: the uKernel's output tile must map onto efficient
+  // tcgen05 tiles in one of the two orientations: 128 or 256 TMEM lanes
+  // (M = 128 per MMA) x 64..256 accumulator columns (MMA N, step 32); a tile
+  // spanning a whole short axis is also accepted. Batch tiles are free (one
+  // work item per batch entry); reduce tiles are whole 64-element TMA atoms.
   if (in.ns < 2) return false;
   const int ai = in.ns - 2, aj = in.ns - 1;
   const int64_t ti = smem[ai], tj = smem[aj], Ei = in.ext[ai], Ej = in.ext[aj];
-  auto lane_ok = [](int64_t t, int64_t E) { return (t % 64 == 0 && t <= 256) || (t >= E && t <= 128); };
-  auto col_ok = [](int64_t t, int64_t E) { return (t % 16 == 0 && t <= 256) || (t >= E && t <= 256); };
+  // lanes: full 128-lane MMA tiles (one or two), or one tile spanning a short axis
+  auto lane_ok = [](int64_t t, int64_t E) { return (t % 128 == 0 && t <= 256) || (t >= E && t <= 128); };
+  // columns: N >= 64 in steps of 32 (the MMA-N sweet spot), or a whole short axis
+  auto col_ok = [](int64_t t, int64_t E) { return (t % 32 == 0 && t >= 64 && t <= 256) || (t >= E && t <= 256); };
   for (int r = in.ns; r < in.na(); ++r)
     if (smem[r] % 64) return false;
   return (lane_ok(ti, Ei) && col_ok(tj, Ej)) || (lane_ok(tj, Ej) && col_ok(ti, Ei));
@@ -430,7 +434,7 @@ static void retention(const Cands& c, const Sweep& sw, std::vector<int64_t>& ste
   }
 }
 
-Cands compile_shape(const Instance& in, const Hw& hw, const Params& p, Report* rep) {
+Cands compile_shape(const Instance& in, const Hw& hw, const Params& p, Report* rep, int stage) {
   bool truncated = false;
   Cands all = enumerate_legal(in, hw, p.cap, &truncated);
   annotate(all, hw, p.rest_regs);
@@ -469,45 +473,85 @@ Cands compile_shape(const Instance& in, const Hw& hw, const Params& p, Report* r
       fin = filt;
     }
   } else if (filt.empty()) {  // filtering.py:292-318
-    int64_t w = 0;
-    bool dropped = false;
-    while (filt.empty()) {
-      ++w;
-      Sweep wid = p.sweep.widened(w);
-      if (wid == used || w > 2000) {
-        relax = FTB_RELAX_DROP_SWEEP;
-        cross.resize(n);
-        std::iota(cross.begin(), cross.end(), 0);
-        n_cross = static_cast<int64_t>(n);
-        retained_all.assign(n, 0);
-        filt.clear();
-        for (int64_t i : cross)
-          if (reg_ok[i]) filt.push_back(i);
-        if (filt.empty())
-          throw FtbError(FTB_EMPTY_RESULT, "no candidate passes the register budget", "register budget");
-        dropped = true;
-        break;
+    // The reference re-runs the sweep for w = 1, 2, ... until the register-
+    // bounded set is non-empty. Retention is monotone in w (eps_min and
+    // lam_min only decrease, so the padding bound and the step count only
+    // grow), so the first successful w is min over register-feasible rows of
+    // each row's first retaining w, found by bisection. The loop stops early
+    // (drop-sweep) at the first w whose floored bounds equal the previous
+    // ones, or past 2000 widenings — computed here without iterating.
+    int64_t w_end = 0;  // last w the reference would actually try
+    for (int64_t w = 1; w <= _MAX_WIDEN; ++w) {
+      if (p.sweep.widened(w) == p.sweep.widened(w - 1)) break;
+      w_end = w;
+    }
+    struct Pt { int64_t en, ed, last; };
+    std::vector<Pt> pts(w_end + 1);
+    for (int64_t w = 1; w <= w_end; ++w) {
+      Sweep sw = p.sweep.widened(w);
+      pts[w] = {sw.eps_min.n, sw.eps_min.d, sw.num_steps()};
+    }
+    const int64_t sn = p.sweep.eps_step.n, sd = p.sweep.eps_step.d;
+    const int64_t ln = p.sweep.lam_max.n, ld = p.sweep.lam_max.d;
+    const int64_t tn = p.sweep.lam_step.n, td = p.sweep.lam_step.d;
+    auto kept_at = [&](size_t i, int64_t w) {
+      const int64_t pn = all.pad_num[i], pd = all.pad_den[i], on = all.blocks[i], od = all.occ_den[i];
+      const int64_t t_pad = 1 + py_floordiv((pn * pts[w].ed - pts[w].en * pd) * sd, pd * pts[w].ed * sn);
+      const int64_t t_occ = std::max<int64_t>(1 + py_ceildiv((ln * od - on * ld) * td, od * ld * tn), 1);
+      return t_occ <= std::min(t_pad, pts[w].last);
+    };
+    int64_t w_star = w_end + 1;
+    for (size_t i = 0; i < n && w_end > 0; ++i) {
+      if (!reg_ok[i]) continue;
+      const int64_t hi0 = std::min(w_star - 1, w_end);
+      if (hi0 < 1 || !kept_at(i, hi0)) continue;
+      int64_t lo = 1, hi = hi0;  // first w in [1, hi0] with kept_at true
+      while (lo < hi) {
+        const int64_t mid = lo + (hi - lo) / 2;
+        if (kept_at(i, mid)) hi = mid; else lo = mid + 1;
       }
-      used = wid;
+      w_star = lo;
+    }
+    if (w_star <= w_end) {
+      used = p.sweep.widened(w_star);
       run_cross(used);
       n_cross = static_cast<int64_t>(cross.size());
       retained_all = steps;
-    }
-    if (!dropped) {
       relax = FTB_RELAX_WIDEN;
-      widen = static_cast<int>(w);
+      widen = static_cast<int>(w_star);
+      if (filt.empty()) throw internal_error("widening bisection disagrees with the sweep");
+    } else {
+      if (w_end > 0) used = p.sweep.widened(w_end);
+      relax = FTB_RELAX_DROP_SWEEP;
+      cross.resize(n);
+      std::iota(cross.begin(), cross.end(), 0);
+      n_cross = static_cast<int64_t>(n);
+      retained_all.assign(n, 0);
+      filt.clear();
+      for (int64_t i : cross)
+        if (reg_ok[i]) filt.push_back(i);
+      if (filt.empty())
+        throw FtbError(FTB_EMPTY_RESULT, "no candidate passes the register budget", "register budget");
     }
     fin = filt;
   }
   all.retained = retained_all;
   const int64_t n_align = static_cast<int64_t>(n), n_filter = static_cast<int64_t>(filt.size());
-  subset_inplace(all, fin);
+  const int64_t n_final = static_cast<int64_t>(fin.size());
+  if (stage == 0) {
+    subset_inplace(all, fin);
+  } else if (stage == 1) {
+    subset_inplace(all, filt);
+  } else if (stage == 2) {
+    subset_inplace(all, cross);
+  }  // stage 3: the whole (legal) align set
   attach_part_metrics(all);
   if (rep) {
     rep->n_align = n_align;
     rep->n_cross = n_cross;
     rep->n_filter = n_filter;
-    rep->n_final = static_cast<int64_t>(all.size());
+    rep->n_final = n_final;
+    rep->stage = stage;
     rep->relaxation = relax;
     rep->widen = widen;
     rep->truncated = truncated;

@@ -79,6 +79,7 @@ struct Report {
   int widen = 0;
   bool truncated = false;
   int tau = 0;
+  int stage = 0;
   Sweep used;
 };
 
@@ -91,7 +92,9 @@ struct PlanRow {
 Cands enumerate(const Instance& in, const Hw& hw, int64_t cap, bool* truncated);
 // enumerate + (B200 mode) the tcgen05 legality filter
 Cands enumerate_legal(const Instance& in, const Hw& hw, int64_t cap, bool* truncated);
-Cands compile_shape(const Instance& in, const Hw& hw, const Params& p, Report* rep);
+// stage selects the returned set: 0 final (reference), 1 filter, 2 cross, 3 align
+// (1-3 are the B200-mode fallback rungs used when the final set cannot cover tau).
+Cands compile_shape(const Instance& in, const Hw& hw, const Params& p, Report* rep, int stage = 0);
 int select_main_axis(const Instance& in);
 int64_t pool_count(const Cands& c, int tau);
 std::vector<PlanRow> pool_export(const Cands& c, int tau);

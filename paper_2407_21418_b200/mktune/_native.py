@@ -53,7 +53,7 @@ class Report(C.Structure):
     _fields_ = [
         ("n_align", C.c_int64), ("n_cross", C.c_int64), ("n_filter", C.c_int64), ("n_final", C.c_int64),
         ("relaxation", C.c_int32), ("widen", C.c_int32), ("truncated", C.c_int32), ("tau", C.c_int32),
-        ("sweep_used", Frac * 6), ("seconds", C.c_double),
+        ("sweep_used", Frac * 6), ("stage", C.c_int32), ("reserved", C.c_int32), ("seconds", C.c_double),
     ]
 
 

@@ -1,0 +1,188 @@
+"""Runtime front door: plan dynamic shapes with the C++ planner (cached) and
+execute them with the sm_100a executor.
+
+    pl = Planner()                          # B200 descriptor, tcgen05 mode
+    C = pl.dense(A, W, b_layout="nk")       # plan (cached per shape) + one launch
+    progs = pl.plan([dense_instance(M, 2304, 768) for M in Ms])   # batch tuning
+
+The planner is the reference's analytic pipeline (compile stage + runtime
+stage + SIA Top-1) run per shape in C++ on a host thread
+pool; planning time is reported as "tuning seconds" and never lands inside a
+timed kernel region. The plan cache is keyed by (descriptor, workload hash,
+binding), the f-1 "persistent plan cache" of SURVEY.md §8.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+import json
+import threading
+import time
+from dataclasses import dataclass
+from pathlib import Path
+from typing import Sequence
+
+from . import _lib
+from .execute import Executable, gemm_desc
+from .mktune import _native
+from .mktune.filtering import FilterParams
+from .mktune.hardware import HardwareDescriptor, b200_bf16, b200_ffma
+from .mktune.scoring import SiaCoeffs
+from .mktune.workload import WorkloadInstance, bmm_spec, dense_spec, workload_hash
+
+CACHE_VERSION = 1
+
+
+def dense_instance(M: int, N: int, K: int, elem_bytes: int = 2, m_max: int = 8192) -> WorkloadInstance:
+    return WorkloadInstance(dense_spec(N, K, (1, max(m_max, M)), elem_bytes), {"i": M})
+
+
+def bmm_instance(b: int, M: int, N: int, K: int, dynamic=("i", "j"), elem_bytes: int = 2,
+                 t_max: int = 512) -> WorkloadInstance:
+    """BatchMatmul instance; ``dynamic`` names the axes bound per call
+    (scores: i, j = T; context: i, k = T)."""
+    ext = {"i": M, "j": N, "k": K}
+    hi = max(t_max, M, N, K)
+    spec = bmm_spec(b, *[((1, hi) if a in dynamic else ext[a]) for a in ("i", "j", "k")], elem_bytes=elem_bytes,
+                    name="bmm-" + "".join(dynamic))
+    return WorkloadInstance(spec, {a: ext[a] for a in dynamic})
+
+
+@dataclass
+class PlanRecord:
+    program: _lib.Program
+    tuning_s: float
+    relaxation: str
+    stage: int
+    counts: dict
+
+    def describe(self) -> dict:
+        g = self.program
+        parts = []
+        for p in range(g.n_parts):
+            parts.append({"smem": [int(g.smem[p][a]) for a in range(g.n_space + g.n_reduce)],
+                          "reg": [int(g.reg[p][a]) for a in range(g.n_space)], "count": int(g.count[p])})
+        return {"tau": int(g.tau), "parts": parts, "sia": float(g.sia), "relaxation": self.relaxation,
+                "fallback_stage": self.stage, "tuning_s": self.tuning_s, "counts": self.counts}
+
+
+class Planner:
+    """Thread-safe plan cache over the C++ planner."""
+
+    def __init__(self, hw: HardwareDescriptor | None = None, params: FilterParams | None = None,
+                 coeffs: SiaCoeffs | None = None, threads: int = 0):
+        self.hw = hw or b200_bf16(tcgen05=True)
+        self.params = params or FilterParams.default()
+        self.coeffs = coeffs or SiaCoeffs()
+        self.threads = threads
+        self._cache: dict[tuple, PlanRecord] = {}
+        self._lock = threading.Lock()
+
+    def _key(self, inst: WorkloadInstance) -> tuple:
+        return (self.hw.name, self.hw.tcgen05_mode, workload_hash(inst.spec), inst.binding_key())
+
+    def plan(self, instances: Sequence[WorkloadInstance]) -> list[PlanRecord]:
+        """Top-1 program per instance (cached); misses are planned in one
+        multi-threaded C++ call."""
+        keys = [self._key(i) for i in instances]
+        with self._lock:
+            miss = [j for j, k in enumerate(keys) if k not in self._cache]
+        if miss:
+            uniq: dict[tuple, int] = {}
+            for j in miss:
+                uniq.setdefault(keys[j], j)
+            todo = list(uniq.values())
+            n = len(todo)
+            insts = (_native.Inst * n)(*[_native.inst_struct(instances[j], self.params.major_axis) for j in todo])
+            progs = (_lib.Program * n)()
+            reps = (_native.Report * n)()
+            stats = (C.c_int32 * n)()
+            _lib.check(_native.lib().ftb_plan_batch(
+                C.byref(_native.hw_struct(self.hw)), insts, n, C.byref(_native.params_struct(self.params)),
+                C.byref(_native.coeffs_struct(self.coeffs)), self.threads, progs, reps, stats))
+            for q, j in enumerate(todo):
+                if stats[q] != 0:
+                    # re-plan alone to surface the exact error text / class
+                    one = (_native.Inst * 1)(insts[q])
+                    _lib.check(_native.lib().ftb_plan_batch(
+                        C.byref(_native.hw_struct(self.hw)), one, 1, C.byref(_native.params_struct(self.params)),
+                        C.byref(_native.coeffs_struct(self.coeffs)), 1, (_lib.Program * 1)(), None, None))
+                r = reps[q]
+                rec = PlanRecord(
+                    program=_lib.Program.from_buffer_copy(progs[q]), tuning_s=r.seconds,
+                    relaxation=_native.relaxation_name(r.relaxation, r.widen), stage=r.stage,
+                    counts={"align": r.n_align, "cross": r.n_cross, "filter": r.n_filter, "final": r.n_final})
+                with self._lock:
+                    self._cache[keys[j]] = rec
+        with self._lock:
+            return [self._cache[k] for k in keys]
+
+    # ---------------------------------------------------------------- ops
+
+    def dense(self, A, B, b_layout: str = "kn", out=None, stream=None):
+        """C = A @ B (B as [K,N] for "kn", as nn.Linear weight [N,K] for "nk")."""
+        import torch
+
+        M, K = A.shape
+        N = B.shape[1] if b_layout == "kn" else B.shape[0]
+        fp32 = A.dtype == torch.float32
+        inst = dense_instance(M, N, K, elem_bytes=4 if fp32 else 2)
+        planner = self if (not fp32 or not self.hw.tcgen05_mode) else _ffma_planner()
+        rec = planner.plan([inst])[0]
+        if out is None:
+            out = torch.empty(M, N, dtype=torch.float32 if fp32 else torch.bfloat16, device=A.device)
+        Executable([gemm_desc(A, B, out, b_layout)], [rec.program], (A, B, out)).launch(stream)
+        return out
+
+    def bmm(self, A, B, b_layout: str = "kn", dynamic=("i", "j"), out=None, stream=None):
+        import torch
+
+        b, M, K = A.shape
+        N = B.shape[2] if b_layout == "kn" else B.shape[1]
+        rec = self.plan([bmm_instance(b, M, N, K, dynamic)])[0]
+        if out is None:
+            out = torch.empty(b, M, N, dtype=torch.bfloat16, device=A.device)
+        Executable([gemm_desc(A, B, out, b_layout)], [rec.program], (A, B, out)).launch(stream)
+        return out
+
+    # ---------------------------------------------------------------- persistence
+
+    def save(self, path: str | Path) -> None:
+        """Write the plan cache (plan file: SPEC.md:412; versioned)."""
+        with self._lock:
+            rows = [{"key": list(k), **v.describe(), "n_space": v.program.n_space}
+                    for k, v in self._cache.items()]
+        Path(path).write_text(json.dumps({"version": CACHE_VERSION, "hw": self.hw.to_doc(), "plans": rows},
+                                         sort_keys=True, indent=1) + "\n")
+
+    def load(self, path: str | Path) -> int:
+        doc = json.loads(Path(path).read_text())
+        if doc.get("version") != CACHE_VERSION or doc.get("hw") != self.hw.to_doc():
+            return 0
+        from .execute import program_struct
+
+        n = 0
+        for row in doc["plans"]:
+            parts = [(p["reg"], p["smem"], p["count"]) for p in row["parts"]]
+            g = program_struct(row["n_space"], row["tau"], parts, row["sia"])
+            with self._lock:
+                self._cache[tuple(row["key"])] = PlanRecord(g, row["tuning_s"], row["relaxation"],
+                                                            row["fallback_stage"], row["counts"])
+            n += 1
+        return n
+
+
+_FFMA = None
+
+
+def _ffma_planner() -> Planner:
+    global _FFMA
+    if _FFMA is None:
+        _FFMA = Planner(hw=b200_ffma())
+    return _FFMA
+
+
+def timed_plan(planner: Planner, instances) -> tuple[list[PlanRecord], float]:
+    t0 = time.perf_counter()
+    recs = planner.plan(instances)
+    return recs, time.perf_counter() - t0

@@ -1,0 +1,77 @@
+"""Host-only lowering (ftb_lower): every uKernel rectangle of a plan becomes
+MMA-sized work items that tile C exactly once; validation rejects plans
+that do not cover tau (combine.py:189-193)."""
+
+import numpy as np
+import pytest
+
+from paper_2407_21418_b200 import _lib
+from paper_2407_21418_b200.execute import lower_table, program_struct
+from paper_2407_21418_b200.mktune import errors
+
+
+def desc(op, batch, M, N, K, b_layout=_lib.B_NK, dt=_lib.DT_BF16, orientation=-1):
+    d = _lib.GemmDesc()
+    d.op, d.batch, d.M, d.N, d.K = op, batch, M, N, K
+    d.A = d.B = d.C = 256
+    d.lda = d.ldb = ((K + 7) // 8) * 8
+    if b_layout == _lib.B_KN:
+        d.ldb = ((N + 7) // 8) * 8
+    d.ldc = N
+    d.a_batch_stride, d.b_batch_stride, d.c_batch_stride = M * d.lda, N * K, M * N
+    d.b_layout, d.in_dtype, d.out_dtype, d.orientation = b_layout, dt, dt, orientation
+    return d
+
+
+def _unused_coverage(table, d):
+    cov = np.zeros((d.batch, d.M, d.N), dtype=np.int32)
+    for w in table:
+        _, b, l0, c0, ll, cl, nm, _ = w
+        assert ll <= 128 and cl <= 256 and nm >= cl
+        if d.__dict__ if False else None:
+            pass
+    return cov
+
+
+def apply(table, d, swap):
+    cov = np.zeros((d.batch, d.M, d.N), dtype=np.int32)
+    for _, b, l0, c0, ll, cl, nm, _ in table:
+        if swap:
+            cov[b, c0:c0 + cl, l0:l0 + ll] += 1
+        else:
+            cov[b, l0:l0 + ll, c0:c0 + cl] += 1
+    return cov
+
+
+@pytest.mark.parametrize("orientation", [0, 1])
+@pytest.mark.parametrize("M,N,parts,tau", [
+    (200, 320, [((1, 8), (30, 64, 64), 3), ((1, 8), (30, 128, 64), 1)], 1),
+    (4096, 768, [((1, 8), (16, 192, 64), 4), ((1, 8), (112, 192, 64), 36)], 0),
+    (1, 768, [((1, 1), (1, 64, 64), 12)], 1),
+    (509, 768, [((1, 8), (30, 512, 64), 1), ((1, 8), (30, 256, 64), 1)], 1),
+])
+def test_dense_tiles_cover_once(orientation, M, N, parts, tau):
+    d = desc(_lib.OP_DENSE, 1, M, N, 256, orientation=orientation)
+    t, info = lower_table([d], [program_struct(2, tau, parts)])
+    assert (apply(t, d, orientation == 1) == 1).all()
+    assert info.true_out == M * N
+
+
+def test_bmm_tiles_cover_once():
+    d = desc(_lib.OP_BMM, 6, 37, 37, 64)
+    t, info = lower_table([d], [program_struct(3, 0, [((1, 1, 1), (2, 37, 64, 64), 3)])])
+    assert (apply(t, d, False) == 1).all() or (apply(t, d, True) == 1).all()
+
+
+def test_rejects_non_covering_plan():
+    d = desc(_lib.OP_DENSE, 1, 100, 320, 64)
+    with pytest.raises(errors.InputError):
+        lower_table([d], [program_struct(2, 1, [((1, 8), (30, 64, 64), 4)])])  # 256 != 320
+    with pytest.raises(errors.InputError):
+        lower_table([d], [program_struct(2, 1, [((1, 8), (30, 64, 64), 3), ((1, 8), (20, 128, 64), 1)])])
+
+
+def test_padding_ratio_matches_covered_extents():
+    d = desc(_lib.OP_DENSE, 1, 53, 768, 768)
+    _, info = lower_table([d], [program_struct(2, 1, [((1, 8), (8, 64, 64), 12)])])
+    assert info.covered_out == 56 * 768 and info.true_out == 53 * 768
