@@ -39,7 +39,7 @@ def test_error_mapping_input_error():
 
 def test_empty_pool_raises_empty_result():
     from paper_2407_21418_b200.mktune import combine, errors, ukernel, workload
-    from tests.golden.cases import dense_doc
+    from cases import dense_doc
 
     inst = workload.WorkloadInstance(workload.parse_workload(dense_doc(64, 64, 4, 100)), {"i": 7})
     k = ukernel.UKernel(reg_tile={"i": 1, "j": 1}, smem_tile={"i": 2, "j": 64, "k": 64},
@@ -55,7 +55,7 @@ def test_empty_pool_raises_empty_result():
 
 def test_missing_metrics():
     from paper_2407_21418_b200.mktune import errors, scoring, ukernel, workload
-    from tests.golden.cases import dense_doc
+    from cases import dense_doc
 
     inst = workload.WorkloadInstance(workload.parse_workload(dense_doc(64, 64, 4, 100)), {"i": 7})
     k = ukernel.UKernel(reg_tile={"i": 1, "j": 1}, smem_tile={"i": 7, "j": 64, "k": 64})

@@ -9,7 +9,7 @@ import pytest
 from _helpers import KATS
 from paper_2407_21418_b200.mktune import combine, filtering, metrics, ukernel, workload
 from paper_2407_21418_b200.mktune.hardware import HardwareDescriptor
-from tests.golden.cases import dense_doc
+from cases import dense_doc
 
 
 def hw80():

@@ -54,6 +54,12 @@ def test_topk_streaming_matches_reference(compiled, cid):
     inst, r = compiled[cid]
     assert select_main_axis(inst) == g["tau"]
     assert plan_pool_size(r.candidates, inst) == g["pool_size"]
+    if g["pool_size"] == 0:  # the reference raises EmptyResultError from build_programs
+        from paper_2407_21418_b200.mktune.errors import EmptyResultError
+
+        with pytest.raises(EmptyResultError):
+            rank_topk(r.candidates, inst, k=10)
+        return
     top = rank_topk(r.candidates, inst, k=10)
     assert top_rows(top, inst) == [t["parts"] for t in g["top10"]]
     assert [fhex(p.sia) for p in top] == [t["sia"] for t in g["top10"]]
