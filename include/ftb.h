@@ -215,6 +215,14 @@ ftb_status ftb_exec_get_info(const ftb_exec* ex, ftb_exec_info* info);
 /* Host copy of the lowered table (int32 x 8 per work item), for tests. */
 ftb_status ftb_exec_export_table(const ftb_exec* ex, int32_t* out, int64_t cap, int64_t* n_out);
 void ftb_exec_destroy(ftb_exec* ex);
+/* Debug: record per-CTA phase timestamps (%globaltimer, ns) for the first 16
+ * items of every CTA on subsequent launches; read back as
+ * [cta][item][6 events] (producer pick, K0 issued, K0 landed, MMA commit,
+ * epilogue start, epilogue release). */
+ftb_status ftb_exec_set_trace(ftb_exec* ex, int32_t enable);
+ftb_status ftb_exec_read_trace(const ftb_exec* ex, uint64_t* out, int64_t cap, int64_t* n_out);
+/* Pipeline shape chosen for the table: {stages, col_stage_bytes, n_acc, acc_cols}. */
+ftb_status ftb_exec_get_config(const ftb_exec* ex, int32_t* out4);
 /* Host-only lowering (no device, no TMA descriptors): the same table
  * ftb_exec_create would upload, for inspection and CPU tests. */
 ftb_status ftb_lower(const ftb_gemm_desc* problems, const ftb_program* programs, int32_t n,

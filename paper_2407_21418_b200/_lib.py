@@ -111,6 +111,9 @@ def lib() -> C.CDLL:
              C.POINTER(ExecInfo)],
         ),
         "ftb_device_sm_count": (i32, []),
+        "ftb_exec_set_trace": (i32, [vp, i32]),
+        "ftb_exec_read_trace": (i32, [vp, C.POINTER(C.c_uint64), i64, C.POINTER(i64)]),
+        "ftb_exec_get_config": (i32, [vp, C.POINTER(i32)]),
     }
     for name, (res, args) in sig.items():
         fn = getattr(L, name)

@@ -23,7 +23,8 @@
 
 namespace ftb {
 
-cudaError_t launch_tc(const DevProblem*, const DevWork*, int32_t, int32_t, cudaStream_t);
+cudaError_t launch_tc(const TcWork*, int32_t, int32_t, TcConfig, cudaStream_t);
+int tc_smem_bytes(const TcConfig& cfg);
 cudaError_t launch_ffma(const DevProblem*, const DevWork*, int32_t, int32_t, cudaStream_t);
 
 namespace {
@@ -164,13 +165,21 @@ void split(int64_t lo, int64_t hi, int64_t maxlen, std::vector<Piece>& out) {
 
 struct ExecImpl {
   std::vector<DevProblem> problems;
-  std::vector<DevWork> work;
+  std::vector<DevMaps> maps;          // tcgen05: TMA descriptors per problem
+  std::vector<DevWork> work;          // logical table (export format, FFMA input)
   DevProblem* d_problems = nullptr;
   DevWork* d_work = nullptr;
+  DevMaps* d_maps = nullptr;
+  TcWork* d_tcwork = nullptr;
+  unsigned long long* d_trace = nullptr;
+  TcConfig cfg{};
   ftb_exec_info info{};
   ~ExecImpl() {
     if (d_problems) cudaFree(d_problems);
     if (d_work) cudaFree(d_work);
+    if (d_maps) cudaFree(d_maps);
+    if (d_tcwork) cudaFree(d_tcwork);
+    if (d_trace) cudaFree(d_trace);
   }
 };
 
@@ -241,19 +250,25 @@ static void build(ExecImpl& ex, const ftb_gemm_desc* probs, const ftb_program* p
     if (!ffma && d.in_dtype != FTB_DT_BF16) throw input_error("unsupported input dtype", "in_dtype");
     if (!ffma && encode) {
       // A: [batch][M][lda], K contiguous. B: [batch][N][ldb] (NK) or [batch][K][ldb] (KN).
-      if (!swap) {
-        encode_map(&P.tm_lane, d.A, d.K, d.M, d.batch, d.lda, d.a_batch_stride, 64, kLaneRows);
-        if (P.b_nk)
-          encode_map(&P.tm_col, d.B, d.K, d.N, d.batch, d.ldb, d.b_batch_stride, 64, kColBoxRows);
-        else
-          encode_map(&P.tm_col, d.B, d.N, d.K, d.batch, d.ldb, d.b_batch_stride, 64, 64);
+      DevMaps m;
+      std::memset(&m, 0, sizeof(m));
+      const void* lane_t = swap ? d.B : d.A;
+      const void* col_t = swap ? d.A : d.B;
+      const int64_t lane_rows = swap ? d.N : d.M, col_rows = swap ? d.M : d.N;
+      const int64_t lane_ld = swap ? d.ldb : d.lda, col_ld = swap ? d.lda : d.ldb;
+      const int64_t lane_bs = swap ? d.b_batch_stride : d.a_batch_stride;
+      const int64_t col_bs = swap ? d.a_batch_stride : d.b_batch_stride;
+      if (!P.lane_mn)
+        encode_map(&m.lane, lane_t, d.K, lane_rows, d.batch, lane_ld, lane_bs, 64, kLaneRows);
+      else
+        encode_map(&m.lane, lane_t, lane_rows, d.K, d.batch, lane_ld, lane_bs, 64, 64);
+      if (!P.col_mn) {
+        for (int q = 0; q < 4; ++q)
+          encode_map(&m.col[q], col_t, d.K, col_rows, d.batch, col_ld, col_bs, 64, 128u >> q);
       } else {
-        if (P.b_nk)
-          encode_map(&P.tm_lane, d.B, d.K, d.N, d.batch, d.ldb, d.b_batch_stride, 64, kLaneRows);
-        else
-          encode_map(&P.tm_lane, d.B, d.N, d.K, d.batch, d.ldb, d.b_batch_stride, 64, 64);
-        encode_map(&P.tm_col, d.A, d.K, d.M, d.batch, d.lda, d.a_batch_stride, 64, kColBoxRows);
+        encode_map(&m.col[0], col_t, col_rows, d.K, d.batch, col_ld, col_bs, 64, 64);
       }
+      ex.maps.push_back(m);
     }
     ex.problems.push_back(P);
 
@@ -304,6 +319,61 @@ static void build(ExecImpl& ex, const ftb_gemm_desc* probs, const ftb_program* p
   if (ex.info.n_work > INT32_MAX) throw input_error("tile table too large", "work");
 }
 
+// Device upload: problems (FFMA) or TMA descriptors + self-contained items
+// (tcgen05), and the per-launch pipeline shape from the widest item.
+static void upload(ExecImpl& I) {
+  FTB_CUDA(cudaMalloc(&I.d_problems, sizeof(DevProblem) * I.problems.size()));
+  FTB_CUDA(cudaMemcpy(I.d_problems, I.problems.data(), sizeof(DevProblem) * I.problems.size(),
+                      cudaMemcpyHostToDevice));
+  if (I.work.empty()) return;
+  if (I.info.kernel == 1) {
+    FTB_CUDA(cudaMalloc(&I.d_work, sizeof(DevWork) * I.work.size()));
+    FTB_CUDA(cudaMemcpy(I.d_work, I.work.data(), sizeof(DevWork) * I.work.size(), cudaMemcpyHostToDevice));
+    return;
+  }
+  FTB_CUDA(cudaMalloc(&I.d_maps, sizeof(DevMaps) * I.maps.size()));
+  FTB_CUDA(cudaMemcpy(I.d_maps, I.maps.data(), sizeof(DevMaps) * I.maps.size(), cudaMemcpyHostToDevice));
+  std::vector<TcWork> tw(I.work.size());
+  int max_n = 16;
+  for (size_t i = 0; i < I.work.size(); ++i) {
+    const DevWork& w = I.work[i];
+    const DevProblem& P = I.problems[w.problem];
+    TcWork& t = tw[i];
+    std::memset(&t, 0, sizeof(t));
+    t.maps = I.d_maps + w.problem;
+    const size_t esz = P.out_f32 ? 4 : 2;
+    t.C = static_cast<char*>(P.C) + static_cast<int64_t>(w.batch) * P.c_bs * esz;
+    t.ldc = P.ldc;
+    t.lane0 = w.lane0;
+    t.col0 = w.col0;
+    t.lane_len = w.lane_len;
+    t.col_len = w.col_len;
+    t.n_mma = w.n_mma;
+    t.num_kb = P.num_kb;
+    t.batch = w.batch;
+    t.flags = (P.swap ? kFlagSwap : 0u) | (P.lane_mn ? kFlagLaneMN : 0u) | (P.col_mn ? kFlagColMN : 0u) |
+              (P.out_f32 ? kFlagOutF32 : 0u);
+    max_n = std::max(max_n, w.n_mma);
+  }
+  FTB_CUDA(cudaMalloc(&I.d_tcwork, sizeof(TcWork) * tw.size()));
+  FTB_CUDA(cudaMemcpy(I.d_tcwork, tw.data(), sizeof(TcWork) * tw.size(), cudaMemcpyHostToDevice));
+  // accumulator slots: the widest item decides the slot width (64/128/256 columns)
+  int acc_cols = max_n <= 64 ? 64 : (max_n <= 128 ? 128 : 256);
+  I.cfg.acc_cols = acc_cols;
+  I.cfg.n_acc = kTmemCols / acc_cols;
+  I.cfg.col_stage_bytes = max_n * kBlockK * 2;
+  I.cfg.stages = 1;
+  for (int s = kMaxStages; s >= 2; --s) {
+    TcConfig c = I.cfg;
+    c.stages = s;
+    if (tc_smem_bytes(c) <= 232448) {
+      I.cfg.stages = s;
+      break;
+    }
+  }
+  I.cfg.trace = nullptr;
+}
+
 }  // namespace ftb
 
 struct ftb_exec {
@@ -322,14 +392,7 @@ ftb_status ftb_exec_create(const ftb_gemm_desc* problems, const ftb_program* pro
     try {
       ftb::build(ex->impl, problems, programs, n, /*encode=*/true);
       auto& I = ex->impl;
-      FTB_CUDA(cudaMalloc(&I.d_problems, sizeof(ftb::DevProblem) * I.problems.size()));
-      FTB_CUDA(cudaMemcpy(I.d_problems, I.problems.data(),
-                          sizeof(ftb::DevProblem) * I.problems.size(), cudaMemcpyHostToDevice));
-      if (!I.work.empty()) {
-        FTB_CUDA(cudaMalloc(&I.d_work, sizeof(ftb::DevWork) * I.work.size()));
-        FTB_CUDA(cudaMemcpy(I.d_work, I.work.data(), sizeof(ftb::DevWork) * I.work.size(),
-                            cudaMemcpyHostToDevice));
-      }
+      ftb::upload(I);
     } catch (...) {
       delete ex;
       throw;
@@ -346,8 +409,8 @@ ftb_status ftb_exec_launch(ftb_exec* ex, void* stream) {
     cudaError_t e = I.info.kernel == 1
                         ? ftb::launch_ffma(I.d_problems, I.d_work, static_cast<int32_t>(I.info.n_work),
                                            static_cast<int32_t>(I.info.n_ctas), s)
-                        : ftb::launch_tc(I.d_problems, I.d_work, static_cast<int32_t>(I.info.n_work),
-                                         static_cast<int32_t>(I.info.n_ctas), s);
+                        : ftb::launch_tc(I.d_tcwork, static_cast<int32_t>(I.info.n_work),
+                                         static_cast<int32_t>(I.info.n_ctas), I.cfg, s);
     if (e != cudaSuccess) throw ftb::cuda_error(std::string("kernel launch: ") + cudaGetErrorString(e));
   });
 }
@@ -372,6 +435,38 @@ ftb_status ftb_exec_export_table(const ftb_exec* ex, int32_t* out, int64_t cap, 
 }
 
 void ftb_exec_destroy(ftb_exec* ex) { delete ex; }
+
+ftb_status ftb_exec_set_trace(ftb_exec* ex, int32_t enable) {
+  return ftb::guarded([&] {
+    if (!ex) throw ftb::input_error("null exec");
+    auto& I = ex->impl;
+    if (I.info.kernel != 0) throw ftb::input_error("tracing is only available for the tcgen05 kernel");
+    if (enable && !I.d_trace) {
+      const size_t n = static_cast<size_t>(I.info.n_ctas) * ftb::kTraceItems * ftb::kTraceEvents;
+      FTB_CUDA(cudaMalloc(&I.d_trace, n * sizeof(unsigned long long)));
+      FTB_CUDA(cudaMemset(I.d_trace, 0, n * sizeof(unsigned long long)));
+    }
+    I.cfg.trace = enable ? I.d_trace : nullptr;
+  });
+}
+
+ftb_status ftb_exec_read_trace(const ftb_exec* ex, uint64_t* out, int64_t cap, int64_t* n_out) {
+  return ftb::guarded([&] {
+    if (!ex || !n_out) throw ftb::input_error("null argument");
+    const auto& I = ex->impl;
+    const int64_t n = I.d_trace ? I.info.n_ctas * ftb::kTraceItems * ftb::kTraceEvents : 0;
+    *n_out = n;
+    if (out && n) FTB_CUDA(cudaMemcpy(out, I.d_trace, sizeof(uint64_t) * std::min(cap, n), cudaMemcpyDeviceToHost));
+  });
+}
+
+ftb_status ftb_exec_get_config(const ftb_exec* ex, int32_t* out4) {
+  return ftb::guarded([&] {
+    if (!ex || !out4) throw ftb::input_error("null argument");
+    const auto& c = ex->impl.cfg;
+    out4[0] = c.stages; out4[1] = c.col_stage_bytes; out4[2] = c.n_acc; out4[3] = c.acc_cols;
+  });
+}
 
 ftb_status ftb_lower(const ftb_gemm_desc* problems, const ftb_program* programs, int32_t n,
                      int32_t* out, int64_t cap, int64_t* n_out, ftb_exec_info* info) {

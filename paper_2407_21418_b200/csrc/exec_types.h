@@ -1,21 +1,17 @@
 // exec_types.h — device-resident tile-schedule table shared by the host
-// lowering (lower.cpp) and the persistent kernels (kernel_tc.cu, kernel_ffma.cu).
+// lowering (exec.cu) and the persistent kernels (kernel_tc.cu, kernel_ffma.cu).
 #pragma once
 #include <cstdint>
 #include <cuda.h>
 
 namespace ftb {
 
-// One GEMM problem as the kernels see it. TMA descriptors are built on the
-// host (cuTensorMapEncodeTiled) and live in global memory next to the table.
+// One GEMM problem as the FFMA kernel and the host see it.
 //   lane operand: the tensor whose rows map to TMEM lanes (MMA M = 128)
 //   col operand : the tensor whose rows map to TMEM columns (MMA N <= 256)
 // orientation 0 (normal): lanes = i (A), cols = j (B)
 // orientation 1 (swap-AB): lanes = j (B), cols = i (A)
-struct alignas(128) DevProblem {
-  CUtensorMap tm_lane;   // box {64, 128, 1} (K-major) or {64, 64, 1} (MN-major)
-  CUtensorMap tm_col;    // box {64, 16, 1}  (K-major) or {64, 64, 1} (MN-major)
-  // Raw views, used by the FFMA kernel and by the epilogue.
+struct DevProblem {
   const void* A;
   const void* B;
   void* C;
@@ -28,10 +24,19 @@ struct alignas(128) DevProblem {
   int32_t out_f32;            // C dtype: 0 bf16, 1 fp32
   int32_t b_nk;               // B stored [N,K]
   int32_t num_kb;             // ceil(K / 64)
-  int32_t pad_[2];
 };
 
-// One work item: an output rectangle of at most 128 lanes x 256 columns.
+// TMA descriptors of one problem for the tcgen05 kernel (64-B aligned).
+//   lane  : box {64, 128} (K-major) or {64 MN, 64 K} (MN-major)
+//   col[q]: K-major boxes of 128 >> q rows (q = 0..3: 128, 64, 32, 16);
+//           MN-major: col[0] = box {64 MN, 64 K}
+struct alignas(64) DevMaps {
+  CUtensorMap lane;
+  CUtensorMap col[4];
+};
+
+// Logical work item (host export format, 8 x int32): an output rectangle of
+// at most 128 lanes x 256 columns of one problem.
 struct alignas(16) DevWork {
   int32_t problem;
   int32_t batch;
@@ -40,17 +45,43 @@ struct alignas(16) DevWork {
   int32_t lane_len;  // valid lanes (<= 128)
   int32_t col_len;   // valid columns (<= 256)
   int32_t n_mma;     // MMA N (multiple of 16; of 64 when col operand is MN-major)
-  int32_t aux;       // FFMA: reg tiles (ri | rj << 16); tcgen05: unused
+  int32_t aux;       // unused (0)
 };
+
+// Self-contained tcgen05 work item (64 B): everything a role needs without a
+// dependent load of the problem record.
+enum : uint32_t { kFlagSwap = 1u, kFlagLaneMN = 2u, kFlagColMN = 4u, kFlagOutF32 = 8u };
+struct alignas(64) TcWork {
+  const DevMaps* maps;
+  void* C;            // element 0 of this batch entry's output matrix
+  int64_t ldc;
+  int32_t lane0, col0;
+  int32_t lane_len, col_len;
+  int32_t n_mma, num_kb;
+  int32_t batch;
+  uint32_t flags;
+  int32_t pad_[2];
+};
+
+// Per-launch pipeline shape, chosen by the host from the table's widest item.
+struct TcConfig {
+  int32_t stages;          // smem ring depth (K blocks of 64)
+  int32_t col_stage_bytes; // bytes reserved per stage for the column operand
+  int32_t n_acc;           // TMEM accumulator slots (2, 4 or 8)
+  int32_t acc_cols;        // columns per slot (512 / n_acc)
+  unsigned long long* trace;  // optional: per-CTA phase timestamps (debug)
+};
+constexpr int kTraceItems = 16;   // items traced per CTA
+constexpr int kTraceEvents = 6;   // see kernel_tc.cu
 
 constexpr int kBlockK = 64;          // one 128-B swizzle atom of bf16 along K
 constexpr int kLaneRows = 128;       // MMA M
 constexpr int kMaxN = 256;           // MMA N upper bound
-constexpr int kStages = 4;
+constexpr int kMaxStages = 8;
 constexpr int kLaneStageBytes = kLaneRows * kBlockK * 2;   // 16 KiB
-constexpr int kColStageBytes = kMaxN * kBlockK * 2;        // 32 KiB
-constexpr int kColBoxRows = 16;                            // K-major col operand box rows
-constexpr int kTmemCols = 512;                             // 2 accumulators x 256 columns
+constexpr int kTmemCols = 512;
 constexpr int kTcThreads = 192;                            // 6 warps
+constexpr int kEpiStageBytes = 4 * 32 * 33 * 4;            // per-warp 32x33 fp32 transpose tiles
+constexpr int kTcSmemBudget = 232448 - 1024;               // max dynamic smem minus align slack
 
 }  // namespace ftb

@@ -2,19 +2,25 @@
 //
 // One launch runs every work item of a lowered tile-schedule table (any mix of
 // problems, uKernel tile sizes and orientations). Each CTA owns one SM and
-// walks its share of the table with three warp roles:
-//   warp 0      TMA producer: per 64-wide K block, one box for the lane operand
-//               (128 rows) and n_mma/16 (K-major) or n_mma/64 (MN-major) boxes
-//               for the column operand, into a 4-stage smem ring (SW128).
-//   warp 1      MMA issuer: one elected thread issues 4 x tcgen05.mma
-//               (M=128, N=n_mma, K=16) per K block into one of two TMEM
-//               accumulators (2 x 256 columns) and commits to mbarriers.
-//   warps 2..5  epilogue: tcgen05.ld 32 columns at a time, bf16/fp32 convert,
-//               predicated stores for ragged uKernel edges; releases the
-//               accumulator so the next item's MMAs overlap this store.
-// The reference has no executor; the semantics it must honour are
+// walks its share of the table (static round-robin over a cost-sorted list)
+// with three warp roles that only meet at mbarriers:
+//   warp 0      TMA producer: per 64-wide K block, one (K-major) or two
+//               (MN-major) boxes for the 128-row lane operand and 1-5 boxes
+//               for the n_mma-row column operand, into an S-stage smem ring
+//               (128-B swizzle). Items are prefetched one ahead.
+//   warp 1      MMA issuer: one thread issues 4 x tcgen05.mma (M=128,
+//               N=n_mma, K=16) per K block into one of n_acc TMEM accumulator
+//               slots, commits each stage back to the producer and each
+//               finished item to the epilogue.
+//   warps 2..5  epilogue: tcgen05.ld 32 columns at a time; normal orientation
+//               stores each lane's row segment with 16-B vector stores;
+//               swap-AB orientation transposes 32x32 blocks through shared
+//               memory so stores are row-contiguous too. Predication only on
+//               ragged uKernel edges; the slot is released to the MMA warp
+//               right after its last tcgen05.ld.
+// The reference has no executor; what it must honour is the
 // ProgramPlan coverage (combine.py:40-55): each work item writes exactly its
-// rectangle of C, and the rectangles of a plan tile C once.
+// rectangle of C and the rectangles of a plan tile C once.
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
 
@@ -23,85 +29,151 @@
 
 namespace ftb {
 
-struct TcSmem {
-  uint64_t full[kStages];
-  uint64_t empty[kStages];
-  uint64_t tfull[2];
-  uint64_t tempty[2];
-  uint32_t tmem_base;
-};
+__device__ __forceinline__ TcWork load_work(const TcWork* __restrict__ work, int w) {
+  TcWork it;
+  const uint4* src = reinterpret_cast<const uint4*>(work + w);
+  uint4* dst = reinterpret_cast<uint4*>(&it);
+#pragma unroll
+  for (int q = 0; q < 4; ++q) dst[q] = __ldg(src + q);
+  return it;
+}
 
-constexpr int kRingBytes = kStages * (kLaneStageBytes + kColStageBytes);
-constexpr int kTcSmemBytes = kRingBytes + 1024 /*align slack*/ + 256 /*barriers*/;
+__device__ __forceinline__ void store_row32(void* C, int64_t off, const float* v, int n, bool f32,
+                                            bool vec_ok) {
+  if (f32) {
+    float* dst = static_cast<float*>(C) + off;
+    if (vec_ok && n == 32) {
+#pragma unroll
+      for (int q = 0; q < 8; ++q)
+        reinterpret_cast<float4*>(dst)[q] = make_float4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
+    } else {
+#pragma unroll
+      for (int e = 0; e < 32; ++e)
+        if (e < n) dst[e] = v[e];
+    }
+  } else {
+    __nv_bfloat16* dst = static_cast<__nv_bfloat16*>(C) + off;
+    if (vec_ok && n == 32) {
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        uint4 pk;
+        uint32_t* pw = reinterpret_cast<uint32_t*>(&pk);
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          __nv_bfloat162 h = __floats2bfloat162_rn(v[q * 8 + 2 * e], v[q * 8 + 2 * e + 1]);
+          pw[e] = *reinterpret_cast<uint32_t*>(&h);
+        }
+        reinterpret_cast<uint4*>(dst)[q] = pk;
+      }
+    } else {
+#pragma unroll
+      for (int e = 0; e < 32; ++e)
+        if (e < n) dst[e] = __float2bfloat16_rn(v[e]);
+    }
+  }
+}
 
-__device__ __forceinline__ void store_out(void* C, int64_t off, float v, int out_f32) {
-  if (out_f32)
-    static_cast<float*>(C)[off] = v;
-  else
-    static_cast<__nv_bfloat16*>(C)[off] = __float2bfloat16_rn(v);
+__device__ __forceinline__ unsigned long long globaltimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+// trace layout: [cta][item < kTraceItems][event] with events
+//   0 producer picked the item      1 producer issued K block 0
+//   2 MMA saw K block 0 land        3 MMA committed the item
+//   4 epilogue saw the accumulator  5 epilogue released it
+__device__ __forceinline__ void trace_ev(const TcConfig& cfg, uint32_t local, int ev) {
+  if (cfg.trace && local < kTraceItems)
+    cfg.trace[(static_cast<size_t>(blockIdx.x) * kTraceItems + local) * kTraceEvents + ev] = globaltimer();
 }
 
 __global__ void __launch_bounds__(kTcThreads, 1)
-    ftb_tc_kernel(const DevProblem* __restrict__ problems, const DevWork* __restrict__ work,
-                  int32_t n_work) {
+    ftb_tc_kernel(const TcWork* __restrict__ work, int32_t n_work, TcConfig cfg) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                              ~static_cast<uintptr_t>(1023));
-  uint8_t* lane_buf = smem;                                  // kStages x 16 KiB
-  uint8_t* col_buf = smem + kStages * kLaneStageBytes;       // kStages x 32 KiB
-  TcSmem* bars = reinterpret_cast<TcSmem*>(smem + kRingBytes);
+  const int S = cfg.stages;
+  uint8_t* lane_buf = smem;                                   // S x 16 KiB
+  uint8_t* col_buf = smem + S * kLaneStageBytes;              // S x col_stage_bytes
+  float* epi_buf = reinterpret_cast<float*>(col_buf + S * cfg.col_stage_bytes);  // 4 x 32x33
+  uint64_t* bars = reinterpret_cast<uint64_t*>(reinterpret_cast<uint8_t*>(epi_buf) + kEpiStageBytes);
+  uint64_t* full = bars;                      // [S]
+  uint64_t* empty = bars + kMaxStages;        // [S]
+  uint64_t* tfull = bars + 2 * kMaxStages;    // [n_acc]
+  uint64_t* tempty = bars + 3 * kMaxStages;   // [n_acc]
+  uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(bars + 4 * kMaxStages);
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
 
   if (threadIdx.x == 0) {
-    for (int s = 0; s < kStages; ++s) {
-      mbar_init(&bars->full[s], 1);
-      mbar_init(&bars->empty[s], 1);
+    for (int s = 0; s < S; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
     }
-    for (int a = 0; a < 2; ++a) {
-      mbar_init(&bars->tfull[a], 1);
-      mbar_init(&bars->tempty[a], 4);  // one arrive per epilogue warp
+    for (int a = 0; a < cfg.n_acc; ++a) {
+      mbar_init(&tfull[a], 1);
+      mbar_init(&tempty[a], 4);  // one arrive per epilogue warp
     }
     fence_barrier_init();
   }
-  if (warp == 2) tmem_alloc<kTmemCols>(&bars->tmem_base);
+  if (warp == 2) tmem_alloc<kTmemCols>(tmem_holder);
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
-  const uint32_t tmem_base = bars->tmem_base;
+  const uint32_t tmem_base = *tmem_holder;
+  const int G = gridDim.x;
 
   if (warp == 0) {
     // ------------------------------------------------------------ producer
     if (lane == 0) {
       uint32_t g = 0;  // global K-block counter (ring position)
-      for (int w = blockIdx.x; w < n_work; w += gridDim.x) {
-        const DevWork it = work[w];
-        const DevProblem& P = problems[it.problem];
-        const CUtensorMap* tl = &P.tm_lane;
-        const CUtensorMap* tc = &P.tm_col;
-        const uint32_t col_bytes = static_cast<uint32_t>(it.n_mma) * kBlockK * 2;
-        for (int kb = 0; kb < P.num_kb; ++kb, ++g) {
-          const uint32_t s = g % kStages;
-          const uint32_t round = g / kStages;
-          mbar_wait(&bars->empty[s], (round & 1) ^ 1);
-          mbar_arrive_expect_tx(&bars->full[s], kLaneStageBytes + col_bytes);
+      uint32_t local = 0;
+      TcWork nxt;
+      if (static_cast<int>(blockIdx.x) < n_work) nxt = load_work(work, blockIdx.x);
+      for (int w = blockIdx.x; w < n_work; w += G, ++local) {
+        const TcWork it = nxt;
+        if (w + G < n_work) {
+          nxt = load_work(work, w + G);
+        }
+        trace_ev(cfg, local, 0);
+        const CUtensorMap* tl = &it.maps->lane;
+        if (w + G < n_work) {
+          tma_prefetch_desc(&nxt.maps->lane);
+          tma_prefetch_desc(&nxt.maps->col[0]);
+        }
+        const bool lane_mn = it.flags & kFlagLaneMN, col_mn = it.flags & kFlagColMN;
+        const uint32_t bytes = kLaneStageBytes + static_cast<uint32_t>(it.n_mma) * kBlockK * 2;
+        for (int kb = 0; kb < it.num_kb; ++kb, ++g) {
+          const uint32_t s = g % S;
+          const uint32_t round = g / S;
+          mbar_wait(&empty[s], (round & 1) ^ 1);
+          mbar_arrive_expect_tx(&full[s], bytes);
           uint8_t* ldst = lane_buf + s * kLaneStageBytes;
-          uint8_t* cdst = col_buf + s * kColStageBytes;
+          uint8_t* cdst = col_buf + s * cfg.col_stage_bytes;
           const int k0 = kb * kBlockK;
-          if (!P.lane_mn) {
-            tma_load_3d(ldst, tl, &bars->full[s], k0, it.lane0, it.batch);
+          if (!lane_mn) {
+            tma_load_3d(ldst, tl, &full[s], k0, it.lane0, it.batch);
           } else {
-            tma_load_3d(ldst, tl, &bars->full[s], it.lane0, k0, it.batch);
-            tma_load_3d(ldst + 8192, tl, &bars->full[s], it.lane0 + 64, k0, it.batch);
+            tma_load_3d(ldst, tl, &full[s], it.lane0, k0, it.batch);
+            tma_load_3d(ldst + 8192, tl, &full[s], it.lane0 + 64, k0, it.batch);
           }
-          if (!P.col_mn) {
-            for (int r = 0; r < it.n_mma; r += kColBoxRows)
-              tma_load_3d(cdst + r * 128, tc, &bars->full[s], k0, it.col0 + r, it.batch);
+          if (!col_mn) {
+            // widest boxes first: 128, 64, 32, 16 rows
+            int r = 0;
+#pragma unroll 1
+            for (int q = 0; q < 4; ++q) {
+              const int rows = 128 >> q;
+              while (it.n_mma - r >= rows) {
+                tma_load_3d(cdst + r * 128, &it.maps->col[q], &full[s], k0, it.col0 + r, it.batch);
+                r += rows;
+              }
+            }
           } else {
             for (int c = 0; c < it.n_mma; c += 64)
-              tma_load_3d(cdst + c * 128, tc, &bars->full[s], it.col0 + c, k0, it.batch);
+              tma_load_3d(cdst + c * 128, &it.maps->col[0], &full[s], it.col0 + c, k0, it.batch);
           }
+          if (kb == 0) trace_ev(cfg, local, 1);
         }
       }
     }
@@ -110,101 +182,97 @@ __global__ void __launch_bounds__(kTcThreads, 1)
     if (lane == 0) {
       uint32_t g = 0;
       uint32_t local = 0;
-      for (int w = blockIdx.x; w < n_work; w += gridDim.x, ++local) {
-        const DevWork it = work[w];
-        const DevProblem& P = problems[it.problem];
-        const uint32_t acc = local & 1;
-        const uint32_t use = local >> 1;
-        mbar_wait(&bars->tempty[acc], (use & 1) ^ 1);
+      TcWork nxt;
+      if (static_cast<int>(blockIdx.x) < n_work) nxt = load_work(work, blockIdx.x);
+      for (int w = blockIdx.x; w < n_work; w += G, ++local) {
+        const TcWork it = nxt;
+        if (w + G < n_work) nxt = load_work(work, w + G);
+        const uint32_t slot = local % cfg.n_acc;
+        const uint32_t use = local / cfg.n_acc;
+        const uint32_t lane_mn = (it.flags & kFlagLaneMN) ? 1u : 0u;
+        const uint32_t col_mn = (it.flags & kFlagColMN) ? 1u : 0u;
+        mbar_wait(&tempty[slot], (use & 1) ^ 1);
         tc_fence_after();
-        const uint32_t tmem_d = tmem_base + acc * kMaxN;
-        const uint32_t idesc =
-            idesc_bf16_f32(kLaneRows, static_cast<uint32_t>(it.n_mma), P.lane_mn, P.col_mn);
-        for (int kb = 0; kb < P.num_kb; ++kb, ++g) {
-          const uint32_t s = g % kStages;
-          const uint32_t round = g / kStages;
-          mbar_wait(&bars->full[s], round & 1);
+        const uint32_t tmem_d = tmem_base + slot * cfg.acc_cols;
+        const uint32_t idesc = idesc_bf16_f32(kLaneRows, static_cast<uint32_t>(it.n_mma), lane_mn, col_mn);
+        for (int kb = 0; kb < it.num_kb; ++kb, ++g) {
+          const uint32_t s = g % S;
+          const uint32_t round = g / S;
+          mbar_wait(&full[s], round & 1);
           tc_fence_after();
+          if (kb == 0) trace_ev(cfg, local, 2);
           const uint32_t la = smem_addr(lane_buf + s * kLaneStageBytes);
-          const uint32_t ca = smem_addr(col_buf + s * kColStageBytes);
+          const uint32_t ca = smem_addr(col_buf + s * cfg.col_stage_bytes);
 #pragma unroll
           for (int kk = 0; kk < kBlockK / 16; ++kk) {
-            const uint64_t adesc = P.lane_mn ? umma_desc_sw128(la + kk * 2048, 8192, 1024)
-                                             : umma_desc_sw128(la + kk * 32, 16, 1024);
-            const uint64_t bdesc = P.col_mn ? umma_desc_sw128(ca + kk * 2048, 8192, 1024)
-                                            : umma_desc_sw128(ca + kk * 32, 16, 1024);
+            const uint64_t adesc = lane_mn ? umma_desc_sw128(la + kk * 2048, 8192, 1024)
+                                           : umma_desc_sw128(la + kk * 32, 16, 1024);
+            const uint64_t bdesc = col_mn ? umma_desc_sw128(ca + kk * 2048, 8192, 1024)
+                                          : umma_desc_sw128(ca + kk * 32, 16, 1024);
             tc_mma_f16(tmem_d, adesc, bdesc, idesc, (kb | kk) != 0);
           }
-          tc_commit(&bars->empty[s]);  // frees the smem slot when these MMAs finish
+          tc_commit(&empty[s]);  // frees the smem slot when these MMAs finish
         }
-        tc_commit(&bars->tfull[acc]);  // accumulator ready for the epilogue
+        tc_commit(&tfull[slot]);  // accumulator ready for the epilogue
+        trace_ev(cfg, local, 3);
       }
     }
   } else {
     // ------------------------------------------------------------ epilogue
     const int quad = warp & 3;  // TMEM lane quadrant this warp may access
+    float* tb = epi_buf + quad * (32 * 33);
     uint32_t local = 0;
-    for (int w = blockIdx.x; w < n_work; w += gridDim.x, ++local) {
-      const DevWork it = work[w];
-      const DevProblem& P = problems[it.problem];
-      const uint32_t acc = local & 1;
-      const uint32_t use = local >> 1;
-      mbar_wait(&bars->tfull[acc], use & 1);
+    TcWork nxt;
+    if (static_cast<int>(blockIdx.x) < n_work) nxt = load_work(work, blockIdx.x);
+    for (int w = blockIdx.x; w < n_work; w += G, ++local) {
+      const TcWork it = nxt;
+      if (w + G < n_work) nxt = load_work(work, w + G);
+      const uint32_t slot = local % cfg.n_acc;
+      const uint32_t use = local / cfg.n_acc;
+      const bool swap = it.flags & kFlagSwap, f32 = it.flags & kFlagOutF32;
+      mbar_wait(&tfull[slot], use & 1);
       tc_fence_after();
-      const int my_lane = quad * 32 + lane;
-      const bool lane_ok = my_lane < it.lane_len;
-      const int64_t cb = static_cast<int64_t>(it.batch) * P.c_bs;
-      if (quad * 32 < it.lane_len) {
-        const uint32_t taddr = tmem_base + (static_cast<uint32_t>(quad * 32) << 16) + acc * kMaxN;
+      if (quad == 0 && lane == 0) trace_ev(cfg, local, 4);
+      const int lane_base = quad * 32;
+      if (lane_base < it.lane_len) {
+        const uint32_t taddr = tmem_base + (static_cast<uint32_t>(lane_base) << 16) + slot * cfg.acc_cols;
+        const int my_lane = lane_base + lane;
         for (int c0 = 0; c0 < it.col_len; c0 += 32) {
-          uint32_t v[32];
-          tmem_ld_32x32b_x32(taddr + c0, v);
+          uint32_t raw[32];
+          tmem_ld_32x32b_x32(taddr + c0, raw);
           tmem_ld_wait();
-          if (lane_ok) {
-            const int ncol = min(32, it.col_len - c0);
-            if (!P.swap) {
-              // lane = row i of C, columns = consecutive j
-              const int64_t row = it.lane0 + my_lane;
-              const int64_t base = cb + row * P.ldc + it.col0 + c0;
-              if (!P.out_f32 && ncol == 32 && (base & 7) == 0) {
-                uint4* dst = reinterpret_cast<uint4*>(static_cast<__nv_bfloat16*>(P.C) + base);
+          float v[32];
 #pragma unroll
-                for (int q = 0; q < 4; ++q) {
-                  uint4 pk;
-                  uint32_t* pw = reinterpret_cast<uint32_t*>(&pk);
+          for (int e = 0; e < 32; ++e) v[e] = __uint_as_float(raw[e]);
+          const int ncol = min(32, it.col_len - c0);
+          if (!swap) {
+            // lane = row of C, TMEM columns = consecutive output columns
+            if (my_lane < it.lane_len) {
+              const int64_t off = static_cast<int64_t>(it.lane0 + my_lane) * it.ldc + it.col0 + c0;
+              store_row32(it.C, off, v, ncol, f32, (off & (f32 ? 3 : 7)) == 0);
+            }
+          } else {
+            // lane = column j of C, TMEM columns = rows i: transpose the 32x32
+            // block in smem, then each thread writes one row segment.
 #pragma unroll
-                  for (int e = 0; e < 4; ++e) {
-                    __nv_bfloat162 h = __floats2bfloat162_rn(__uint_as_float(v[q * 8 + 2 * e]),
-                                                             __uint_as_float(v[q * 8 + 2 * e + 1]));
-                    pw[e] = *reinterpret_cast<uint32_t*>(&h);
-                  }
-                  dst[q] = pk;
-                }
-              } else if (P.out_f32 && ncol == 32 && (base & 3) == 0) {
-                float4* dst = reinterpret_cast<float4*>(static_cast<float*>(P.C) + base);
+            for (int e = 0; e < 32; ++e) tb[e * 33 + lane] = v[e];
+            __syncwarp();
+            float r[32];
 #pragma unroll
-                for (int q = 0; q < 8; ++q)
-                  dst[q] = make_float4(__uint_as_float(v[4 * q]), __uint_as_float(v[4 * q + 1]),
-                                       __uint_as_float(v[4 * q + 2]), __uint_as_float(v[4 * q + 3]));
-              } else {
-#pragma unroll
-                for (int e = 0; e < 32; ++e)
-                  if (e < ncol) store_out(P.C, base + e, __uint_as_float(v[e]), P.out_f32);
-              }
-            } else {
-              // lane = column j of C, TMEM columns = consecutive rows i
-              const int64_t col = it.lane0 + my_lane;
-              const int64_t base = cb + static_cast<int64_t>(it.col0 + c0) * P.ldc + col;
-#pragma unroll
-              for (int e = 0; e < 32; ++e)
-                if (e < ncol) store_out(P.C, base + e * P.ldc, __uint_as_float(v[e]), P.out_f32);
+            for (int x = 0; x < 32; ++x) r[x] = tb[lane * 33 + x];
+            __syncwarp();
+            const int nj = min(32, it.lane_len - lane_base);
+            if (lane < ncol) {
+              const int64_t off = static_cast<int64_t>(it.col0 + c0 + lane) * it.ldc + it.lane0 + lane_base;
+              store_row32(it.C, off, r, nj, f32, (off & (f32 ? 3 : 7)) == 0);
             }
           }
         }
       }
       tc_fence_before();
       __syncwarp();
-      if (lane == 0) mbar_arrive(&bars->tempty[acc]);
+      if (lane == 0) mbar_arrive(&tempty[slot]);
+      if (quad == 0 && lane == 0) trace_ev(cfg, local, 5);
     }
   }
 
@@ -216,17 +284,23 @@ __global__ void __launch_bounds__(kTcThreads, 1)
   }
 }
 
-cudaError_t launch_tc(const DevProblem* problems, const DevWork* work, int32_t n_work,
-                      int32_t n_ctas, cudaStream_t stream) {
-  static bool configured = false;
-  if (!configured) {
+int tc_smem_bytes(const TcConfig& cfg) {
+  return 1024 + cfg.stages * (kLaneStageBytes + cfg.col_stage_bytes) + kEpiStageBytes +
+         (4 * kMaxStages + 2) * 8;
+}
+
+cudaError_t launch_tc(const TcWork* work, int32_t n_work, int32_t n_ctas, TcConfig cfg,
+                      cudaStream_t stream) {
+  static int configured = 0;
+  const int smem = tc_smem_bytes(cfg);
+  if (smem > configured) {
     cudaError_t e = cudaFuncSetAttribute(ftb_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         kTcSmemBytes);
+                                         232448);
     if (e != cudaSuccess) return e;
-    configured = true;
+    configured = 232448;
   }
   if (n_work == 0) return cudaSuccess;
-  ftb_tc_kernel<<<n_ctas, kTcThreads, kTcSmemBytes, stream>>>(problems, work, n_work);
+  ftb_tc_kernel<<<n_ctas, kTcThreads, smem, stream>>>(work, n_work, cfg);
   return cudaGetLastError();
 }
 

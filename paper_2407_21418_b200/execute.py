@@ -169,6 +169,26 @@ class Executable:
         s = stream if stream is not None else torch.cuda.current_stream()
         _lib.check(_lib.lib().ftb_exec_launch(self._h, C.c_void_p(s.cuda_stream)))
 
+    def config(self) -> dict:
+        """Pipeline shape chosen for this table (tcgen05 kernel)."""
+        out = (C.c_int32 * 4)()
+        _lib.check(_lib.lib().ftb_exec_get_config(self._h, out))
+        return {"stages": out[0], "col_stage_bytes": out[1], "n_acc": out[2], "acc_cols": out[3]}
+
+    def set_trace(self, enable: bool = True) -> None:
+        _lib.check(_lib.lib().ftb_exec_set_trace(self._h, 1 if enable else 0))
+
+    def read_trace(self):
+        """[n_ctas, 16 items, 6 events] of %globaltimer ns (0 = not reached)."""
+        import numpy as np
+
+        L = _lib.lib()
+        n = C.c_int64()
+        _lib.check(L.ftb_exec_read_trace(self._h, None, 0, C.byref(n)))
+        out = np.zeros(n.value, dtype=np.uint64)
+        _lib.check(L.ftb_exec_read_trace(self._h, out.ctypes.data_as(C.POINTER(C.c_uint64)), n.value, C.byref(n)))
+        return out.reshape(-1, 16, 6)
+
     def table(self):
         """The lowered work items as an int32 numpy array [n_work, 8]."""
         import numpy as np
