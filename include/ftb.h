@@ -221,7 +221,8 @@ void ftb_exec_destroy(ftb_exec* ex);
  * epilogue start, epilogue release). */
 ftb_status ftb_exec_set_trace(ftb_exec* ex, int32_t enable);
 ftb_status ftb_exec_read_trace(const ftb_exec* ex, uint64_t* out, int64_t cap, int64_t* n_out);
-/* Pipeline shape chosen for the table: {stages, col_stage_bytes, n_acc, acc_cols}. */
+/* Pipeline shapes chosen for the table, 10 ints: single-CTA kernel {stages,
+ * col_stage_bytes, n_acc, acc_cols}, CTA-pair kernel {same}, n_singles, n_pairs. */
 ftb_status ftb_exec_get_config(const ftb_exec* ex, int32_t* out4);
 /* Host-only lowering (no device, no TMA descriptors): the same table
  * ftb_exec_create would upload, for inspection and CPU tests. */

@@ -208,18 +208,35 @@ ftb_status ftb_plan_batch(const ftb_hw* hw, const ftb_instance* insts, int32_t n
           Instance in = Instance::from_c(insts[i]);
           Report r;
           // Parity mode ranks the final set only (an empty pool raises, as
-          // combine.py:183-188 does). B200 mode falls back to the filter,
-          // cross and align sets when no final-set combination covers tau.
-          const int last = h.legality ? 3 : 0;
-          for (int stage = 0;; ++stage) {
-            Cands c = compile_shape(in, h, q, &r, stage);
-            try {
-              auto top = rank_topk(c, r.tau, *coeffs, 1, false);
-              if (top.empty()) throw FtbError(FTB_EMPTY_RESULT, "empty program pool", "program pool");
-              fill_program(c, r.tau, top[0].first, top[0].second, &out[i]);
-              break;
-            } catch (const FtbError& e) {
-              if (e.code != FTB_EMPTY_RESULT || stage >= last) throw;
+          // combine.py:183-188 does). B200 mode walks a documented fallback
+          // ladder when no combination covers tau: ranked set final -> filter
+          // -> cross -> align; then the same with the main-axis tile relaxed
+          // (any size <= 256, padded inside the MMA tile); then parity mode.
+          struct Rung { int legality, relax; };
+          std::vector<Rung> rungs;
+          if (h.legality) {
+            rungs = {{1, -1}, {1, select_main_axis(in)}, {0, -1}};
+          } else {
+            rungs = {{0, -1}};
+          }
+          bool done = false;
+          for (size_t ri = 0; ri < rungs.size() && !done; ++ri) {
+            Hw hq = h;
+            hq.legality = rungs[ri].legality;
+            hq.relax_tau = rungs[ri].relax;
+            const int last = h.legality ? 3 : 0;
+            for (int stage = 0; stage <= last && !done; ++stage) {
+              try {
+                Cands c = compile_shape(in, hq, q, &r, stage);
+                auto top = rank_topk(c, r.tau, *coeffs, 1, false);
+                if (top.empty()) throw FtbError(FTB_EMPTY_RESULT, "empty program pool", "program pool");
+                fill_program(c, r.tau, top[0].first, top[0].second, &out[i]);
+                r.stage = stage + 4 * static_cast<int>(ri);
+                done = true;
+              } catch (const FtbError& e) {
+                const bool last_try = (ri + 1 == rungs.size()) && stage == last;
+                if (e.code != FTB_EMPTY_RESULT || last_try) throw;
+              }
             }
           }
           fill_report(r, secs_since(t0), reps ? &reps[i] : nullptr);

@@ -1,0 +1,116 @@
+// epilogue.cuh — shared epilogue helpers of the tcgen05 kernels: row-segment
+// stores (16-B vectorised when the destination is aligned and the segment is
+// full, element-predicated on ragged uKernel edges) and %globaltimer.
+#pragma once
+#include <cuda_bf16.h>
+#include <cstdint>
+
+namespace ftb {
+
+__device__ __forceinline__ bool aligned16(const void* C, int64_t off, bool f32) {
+  return ((reinterpret_cast<uintptr_t>(C) + static_cast<uintptr_t>(off) * (f32 ? 4u : 2u)) & 15u) == 0;
+}
+
+__device__ __forceinline__ void store_row32(void* C, int64_t off, const float* v, int n, bool f32,
+                                            bool vec_ok) {
+  if (f32) {
+    float* dst = static_cast<float*>(C) + off;
+    if (vec_ok && n == 32) {
+#pragma unroll
+      for (int q = 0; q < 8; ++q)
+        reinterpret_cast<float4*>(dst)[q] = make_float4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
+    } else {
+#pragma unroll
+      for (int e = 0; e < 32; ++e)
+        if (e < n) dst[e] = v[e];
+    }
+  } else {
+    __nv_bfloat16* dst = static_cast<__nv_bfloat16*>(C) + off;
+    if (vec_ok && n == 32) {
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        uint4 pk;
+        uint32_t* pw = reinterpret_cast<uint32_t*>(&pk);
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          __nv_bfloat162 h = __floats2bfloat162_rn(v[q * 8 + 2 * e], v[q * 8 + 2 * e + 1]);
+          pw[e] = *reinterpret_cast<uint32_t*>(&h);
+        }
+        reinterpret_cast<uint4*>(dst)[q] = pk;
+      }
+    } else {
+#pragma unroll
+      for (int e = 0; e < 32; ++e)
+        if (e < n) dst[e] = __float2bfloat16_rn(v[e]);
+    }
+  }
+}
+
+// Store a 32 x 32 fp32 block that a warp holds in registers — one ROW of C
+// per lane (lane_is_row) or one COLUMN of C per lane — to C[row0.., col0..]
+// (clipped to nrows x ncols). The block goes through a padded smem tile
+// (32 x 33 fp32, conflict-free both ways); each lane then writes 8
+// consecutive elements of one row per pass, so one warp store instruction
+// covers 8 rows x 8 elements x 4 lanes = 8 full 64-B (bf16) row segments
+// instead of 32 scattered 16-B pieces.
+__device__ __forceinline__ void store_block32(float* tb, const float (&v)[32], bool lane_is_row, void* C,
+                                              int64_t ldc, int64_t row0, int64_t col0, int nrows, int ncols,
+                                              bool f32) {
+  const int lane = threadIdx.x & 31;
+  if (lane_is_row) {
+#pragma unroll
+    for (int x = 0; x < 32; ++x) tb[lane * 33 + x] = v[x];
+  } else {
+#pragma unroll
+    for (int x = 0; x < 32; ++x) tb[x * 33 + lane] = v[x];
+  }
+  __syncwarp();
+  const int cq = (lane & 3) * 8;
+#pragma unroll
+  for (int p = 0; p < 4; ++p) {
+    const int r = (lane >> 2) + 8 * p;
+    if (r < nrows && cq < ncols) {
+      float e[8];
+#pragma unroll
+      for (int q = 0; q < 8; ++q) e[q] = tb[r * 33 + cq + q];
+      const int64_t off = (row0 + r) * ldc + col0 + cq;
+      const int n = min(8, ncols - cq);
+      if (f32) {
+        float* dst = static_cast<float*>(C) + off;
+        if (n == 8 && ((reinterpret_cast<uintptr_t>(dst) & 15u) == 0)) {
+          reinterpret_cast<float4*>(dst)[0] = make_float4(e[0], e[1], e[2], e[3]);
+          reinterpret_cast<float4*>(dst)[1] = make_float4(e[4], e[5], e[6], e[7]);
+        } else {
+#pragma unroll
+          for (int q = 0; q < 8; ++q)
+            if (q < n) dst[q] = e[q];
+        }
+      } else {
+        __nv_bfloat16* dst = static_cast<__nv_bfloat16*>(C) + off;
+        if (n == 8 && ((reinterpret_cast<uintptr_t>(dst) & 15u) == 0)) {
+          uint4 pk;
+          uint32_t* pw = reinterpret_cast<uint32_t*>(&pk);
+#pragma unroll
+          for (int q = 0; q < 4; ++q) {
+            __nv_bfloat162 h = __floats2bfloat162_rn(e[2 * q], e[2 * q + 1]);
+            pw[q] = *reinterpret_cast<uint32_t*>(&h);
+          }
+          *reinterpret_cast<uint4*>(dst) = pk;
+        } else {
+#pragma unroll
+          for (int q = 0; q < 8; ++q)
+            if (q < n) dst[q] = __float2bfloat16_rn(e[q]);
+        }
+      }
+    }
+  }
+  __syncwarp();
+}
+
+__device__ __forceinline__ unsigned long long globaltimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+
+}  // namespace ftb

@@ -13,6 +13,9 @@
 #include <cudaTypedefs.h>
 
 #include <algorithm>
+#include <array>
+#include <cstdlib>
+#include <map>
 #include <cstring>
 #include <mutex>
 #include <string>
@@ -24,6 +27,7 @@
 namespace ftb {
 
 cudaError_t launch_tc(const TcWork*, int32_t, int32_t, TcConfig, cudaStream_t);
+cudaError_t launch_tc2(const TcPair*, int32_t, int32_t, TcConfig, cudaStream_t);
 int tc_smem_bytes(const TcConfig& cfg);
 cudaError_t launch_ffma(const DevProblem*, const DevWork*, int32_t, int32_t, cudaStream_t);
 
@@ -171,14 +175,18 @@ struct ExecImpl {
   DevWork* d_work = nullptr;
   DevMaps* d_maps = nullptr;
   TcWork* d_tcwork = nullptr;
+  TcPair* d_tcpairs = nullptr;
   unsigned long long* d_trace = nullptr;
-  TcConfig cfg{};
+  TcConfig cfg{};    // single-CTA kernel (K1)
+  TcConfig cfg2{};   // CTA-pair kernel (K1b)
+  int64_t n_singles = 0, n_pairs = 0, ctas1 = 0, ctas2 = 0;
   ftb_exec_info info{};
   ~ExecImpl() {
     if (d_problems) cudaFree(d_problems);
     if (d_work) cudaFree(d_work);
     if (d_maps) cudaFree(d_maps);
     if (d_tcwork) cudaFree(d_tcwork);
+    if (d_tcpairs) cudaFree(d_tcpairs);
     if (d_trace) cudaFree(d_trace);
   }
 };
@@ -333,16 +341,62 @@ static void upload(ExecImpl& I) {
   }
   FTB_CUDA(cudaMalloc(&I.d_maps, sizeof(DevMaps) * I.maps.size()));
   FTB_CUDA(cudaMemcpy(I.d_maps, I.maps.data(), sizeof(DevMaps) * I.maps.size(), cudaMemcpyHostToDevice));
-  std::vector<TcWork> tw(I.work.size());
+  auto flags_of = [](const DevProblem& P) {
+    return (P.swap ? kFlagSwap : 0u) | (P.lane_mn ? kFlagLaneMN : 0u) | (P.col_mn ? kFlagColMN : 0u) |
+           (P.out_f32 ? kFlagOutF32 : 0u);
+  };
+  auto c_of = [](const DevProblem& P, int32_t batch) {
+    const size_t esz = P.out_f32 ? 4 : 2;
+    return static_cast<void*>(static_cast<char*>(P.C) + static_cast<int64_t>(batch) * P.c_bs * esz);
+  };
+  // CTA pairs: logical items of one problem/batch with the same column range
+  // share the column operand; group them (in cost order) two by two.
+  const char* env = std::getenv("FTB_PAIR");
+  const bool pairing = !(env && env[0] == '0');
+  std::vector<int8_t> paired(I.work.size(), 0);
+  std::vector<TcPair> pairs;
+  if (pairing) {
+    std::map<std::array<int32_t, 4>, int64_t> open;  // key -> first unpaired item
+    for (size_t i = 0; i < I.work.size(); ++i) {
+      const DevWork& w = I.work[i];
+      const std::array<int32_t, 4> key{w.problem, w.batch, w.col0, w.col_len};
+      auto it = open.find(key);
+      if (it == open.end()) {
+        open.emplace(key, static_cast<int64_t>(i));
+        continue;
+      }
+      const DevWork& a = I.work[it->second];
+      const DevProblem& P = I.problems[w.problem];
+      TcPair t;
+      std::memset(&t, 0, sizeof(t));
+      t.maps = I.d_maps + w.problem;
+      t.C = c_of(P, w.batch);
+      t.ldc = P.ldc;
+      t.lane0[0] = a.lane0;
+      t.lane_len[0] = a.lane_len;
+      t.lane0[1] = w.lane0;
+      t.lane_len[1] = w.lane_len;
+      t.col0 = w.col0;
+      t.col_len = w.col_len;
+      t.n_mma = static_cast<int32_t>(round_up(w.col_len, P.col_mn ? 128 : 32));
+      t.num_kb = P.num_kb;
+      t.batch = w.batch;
+      t.flags = flags_of(P);
+      pairs.push_back(t);
+      paired[it->second] = paired[i] = 1;
+      open.erase(it);
+    }
+  }
+  std::vector<TcWork> tw;
   int max_n = 16;
   for (size_t i = 0; i < I.work.size(); ++i) {
+    if (paired[i]) continue;
     const DevWork& w = I.work[i];
     const DevProblem& P = I.problems[w.problem];
-    TcWork& t = tw[i];
+    TcWork t;
     std::memset(&t, 0, sizeof(t));
     t.maps = I.d_maps + w.problem;
-    const size_t esz = P.out_f32 ? 4 : 2;
-    t.C = static_cast<char*>(P.C) + static_cast<int64_t>(w.batch) * P.c_bs * esz;
+    t.C = c_of(P, w.batch);
     t.ldc = P.ldc;
     t.lane0 = w.lane0;
     t.col0 = w.col0;
@@ -351,26 +405,45 @@ static void upload(ExecImpl& I) {
     t.n_mma = w.n_mma;
     t.num_kb = P.num_kb;
     t.batch = w.batch;
-    t.flags = (P.swap ? kFlagSwap : 0u) | (P.lane_mn ? kFlagLaneMN : 0u) | (P.col_mn ? kFlagColMN : 0u) |
-              (P.out_f32 ? kFlagOutF32 : 0u);
+    t.flags = flags_of(P);
     max_n = std::max(max_n, w.n_mma);
+    tw.push_back(t);
   }
-  FTB_CUDA(cudaMalloc(&I.d_tcwork, sizeof(TcWork) * tw.size()));
-  FTB_CUDA(cudaMemcpy(I.d_tcwork, tw.data(), sizeof(TcWork) * tw.size(), cudaMemcpyHostToDevice));
-  // accumulator slots: the widest item decides the slot width (64/128/256 columns)
-  int acc_cols = max_n <= 64 ? 64 : (max_n <= 128 ? 128 : 256);
-  I.cfg.acc_cols = acc_cols;
-  I.cfg.n_acc = kTmemCols / acc_cols;
-  I.cfg.col_stage_bytes = max_n * kBlockK * 2;
-  I.cfg.stages = 1;
-  for (int s = kMaxStages; s >= 2; --s) {
-    TcConfig c = I.cfg;
-    c.stages = s;
-    if (tc_smem_bytes(c) <= 232448) {
-      I.cfg.stages = s;
-      break;
+  I.n_singles = static_cast<int64_t>(tw.size());
+  I.n_pairs = static_cast<int64_t>(pairs.size());
+  if (!tw.empty()) {
+    FTB_CUDA(cudaMalloc(&I.d_tcwork, sizeof(TcWork) * tw.size()));
+    FTB_CUDA(cudaMemcpy(I.d_tcwork, tw.data(), sizeof(TcWork) * tw.size(), cudaMemcpyHostToDevice));
+  }
+  if (!pairs.empty()) {
+    FTB_CUDA(cudaMalloc(&I.d_tcpairs, sizeof(TcPair) * pairs.size()));
+    FTB_CUDA(cudaMemcpy(I.d_tcpairs, pairs.data(), sizeof(TcPair) * pairs.size(), cudaMemcpyHostToDevice));
+  }
+  int sms = device_sms();
+  if (sms <= 0) sms = 148;
+  I.ctas1 = std::min<int64_t>(I.n_singles, sms);
+  I.ctas2 = 2 * std::min<int64_t>(I.n_pairs, sms / 2);
+  I.info.n_ctas = std::max(I.ctas1, I.ctas2);
+  auto shape_cfg = [](TcConfig& c, int max_cols, int col_rows) {
+    // accumulator slots: the widest item decides the slot width (64/128/256 columns)
+    c.acc_cols = max_cols <= 64 ? 64 : (max_cols <= 128 ? 128 : 256);
+    c.n_acc = kTmemCols / c.acc_cols;
+    c.col_stage_bytes = col_rows * kBlockK * 2;
+    c.stages = 1;
+    for (int s = kMaxStages; s >= 2; --s) {
+      TcConfig t = c;
+      t.stages = s;
+      if (tc_smem_bytes(t) <= 232448) {
+        c.stages = s;
+        break;
+      }
     }
-  }
+    c.trace = nullptr;
+  };
+  shape_cfg(I.cfg, max_n, max_n);
+  int max_np = 32;
+  for (const TcPair& t : pairs) max_np = std::max(max_np, t.n_mma);
+  shape_cfg(I.cfg2, max_np, max_np / 2);
   I.cfg.trace = nullptr;
 }
 
@@ -409,8 +482,11 @@ ftb_status ftb_exec_launch(ftb_exec* ex, void* stream) {
     cudaError_t e = I.info.kernel == 1
                         ? ftb::launch_ffma(I.d_problems, I.d_work, static_cast<int32_t>(I.info.n_work),
                                            static_cast<int32_t>(I.info.n_ctas), s)
-                        : ftb::launch_tc(I.d_tcwork, static_cast<int32_t>(I.info.n_work),
-                                         static_cast<int32_t>(I.info.n_ctas), I.cfg, s);
+                        : cudaSuccess;
+    if (e == cudaSuccess && I.info.kernel == 0 && I.n_pairs)
+      e = ftb::launch_tc2(I.d_tcpairs, static_cast<int32_t>(I.n_pairs), static_cast<int32_t>(I.ctas2), I.cfg2, s);
+    if (e == cudaSuccess && I.info.kernel == 0 && I.n_singles)
+      e = ftb::launch_tc(I.d_tcwork, static_cast<int32_t>(I.n_singles), static_cast<int32_t>(I.ctas1), I.cfg, s);
     if (e != cudaSuccess) throw ftb::cuda_error(std::string("kernel launch: ") + cudaGetErrorString(e));
   });
 }
@@ -463,8 +539,14 @@ ftb_status ftb_exec_read_trace(const ftb_exec* ex, uint64_t* out, int64_t cap, i
 ftb_status ftb_exec_get_config(const ftb_exec* ex, int32_t* out4) {
   return ftb::guarded([&] {
     if (!ex || !out4) throw ftb::input_error("null argument");
-    const auto& c = ex->impl.cfg;
-    out4[0] = c.stages; out4[1] = c.col_stage_bytes; out4[2] = c.n_acc; out4[3] = c.acc_cols;
+    const auto& I = ex->impl;
+    const ftb::TcConfig* cs[2] = {&I.cfg, &I.cfg2};
+    for (int k = 0; k < 2; ++k) {
+      out4[4 * k + 0] = cs[k]->stages; out4[4 * k + 1] = cs[k]->col_stage_bytes;
+      out4[4 * k + 2] = cs[k]->n_acc; out4[4 * k + 3] = cs[k]->acc_cols;
+    }
+    out4[8] = static_cast<int32_t>(I.n_singles);
+    out4[9] = static_cast<int32_t>(I.n_pairs);
   });
 }
 

@@ -63,6 +63,21 @@ struct alignas(64) TcWork {
   int32_t pad_[2];
 };
 
+// CTA-pair work item (64 B): two 128-lane slabs (one per CTA of a cluster
+// pair) that share the column operand; N = n_mma columns, each CTA stages
+// N/2 of them. lane_len[r] == 0 marks an empty half (leftover single).
+struct alignas(64) TcPair {
+  const DevMaps* maps;
+  void* C;
+  int64_t ldc;
+  int32_t lane0[2];
+  int32_t lane_len[2];
+  int32_t col0, col_len;
+  int32_t n_mma, num_kb;
+  int32_t batch;
+  uint32_t flags;
+};
+
 // Per-launch pipeline shape, chosen by the host from the table's widest item.
 struct TcConfig {
   int32_t stages;          // smem ring depth (K blocks of 64)

@@ -26,6 +26,7 @@
 
 #include "exec_types.h"
 #include "ptx.cuh"
+#include "epilogue.cuh"
 
 namespace ftb {
 
@@ -38,46 +39,6 @@ __device__ __forceinline__ TcWork load_work(const TcWork* __restrict__ work, int
   return it;
 }
 
-__device__ __forceinline__ void store_row32(void* C, int64_t off, const float* v, int n, bool f32,
-                                            bool vec_ok) {
-  if (f32) {
-    float* dst = static_cast<float*>(C) + off;
-    if (vec_ok && n == 32) {
-#pragma unroll
-      for (int q = 0; q < 8; ++q)
-        reinterpret_cast<float4*>(dst)[q] = make_float4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
-    } else {
-#pragma unroll
-      for (int e = 0; e < 32; ++e)
-        if (e < n) dst[e] = v[e];
-    }
-  } else {
-    __nv_bfloat16* dst = static_cast<__nv_bfloat16*>(C) + off;
-    if (vec_ok && n == 32) {
-#pragma unroll
-      for (int q = 0; q < 4; ++q) {
-        uint4 pk;
-        uint32_t* pw = reinterpret_cast<uint32_t*>(&pk);
-#pragma unroll
-        for (int e = 0; e < 4; ++e) {
-          __nv_bfloat162 h = __floats2bfloat162_rn(v[q * 8 + 2 * e], v[q * 8 + 2 * e + 1]);
-          pw[e] = *reinterpret_cast<uint32_t*>(&h);
-        }
-        reinterpret_cast<uint4*>(dst)[q] = pk;
-      }
-    } else {
-#pragma unroll
-      for (int e = 0; e < 32; ++e)
-        if (e < n) dst[e] = __float2bfloat16_rn(v[e]);
-    }
-  }
-}
-
-__device__ __forceinline__ unsigned long long globaltimer() {
-  unsigned long long t;
-  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
-  return t;
-}
 // trace layout: [cta][item < kTraceItems][event] with events
 //   0 producer picked the item      1 producer issued K block 0
 //   2 MMA saw K block 0 land        3 MMA committed the item
@@ -236,7 +197,6 @@ __global__ void __launch_bounds__(kTcThreads, 1)
       const int lane_base = quad * 32;
       if (lane_base < it.lane_len) {
         const uint32_t taddr = tmem_base + (static_cast<uint32_t>(lane_base) << 16) + slot * cfg.acc_cols;
-        const int my_lane = lane_base + lane;
         for (int c0 = 0; c0 < it.col_len; c0 += 32) {
           uint32_t raw[32];
           tmem_ld_32x32b_x32(taddr + c0, raw);
@@ -245,28 +205,11 @@ __global__ void __launch_bounds__(kTcThreads, 1)
 #pragma unroll
           for (int e = 0; e < 32; ++e) v[e] = __uint_as_float(raw[e]);
           const int ncol = min(32, it.col_len - c0);
-          if (!swap) {
-            // lane = row of C, TMEM columns = consecutive output columns
-            if (my_lane < it.lane_len) {
-              const int64_t off = static_cast<int64_t>(it.lane0 + my_lane) * it.ldc + it.col0 + c0;
-              store_row32(it.C, off, v, ncol, f32, (off & (f32 ? 3 : 7)) == 0);
-            }
-          } else {
-            // lane = column j of C, TMEM columns = rows i: transpose the 32x32
-            // block in smem, then each thread writes one row segment.
-#pragma unroll
-            for (int e = 0; e < 32; ++e) tb[e * 33 + lane] = v[e];
-            __syncwarp();
-            float r[32];
-#pragma unroll
-            for (int x = 0; x < 32; ++x) r[x] = tb[lane * 33 + x];
-            __syncwarp();
-            const int nj = min(32, it.lane_len - lane_base);
-            if (lane < ncol) {
-              const int64_t off = static_cast<int64_t>(it.col0 + c0 + lane) * it.ldc + it.lane0 + lane_base;
-              store_row32(it.C, off, r, nj, f32, (off & (f32 ? 3 : 7)) == 0);
-            }
-          }
+          const int nlane = min(32, it.lane_len - lane_base);
+          if (!swap)  // lanes = rows of C, TMEM columns = output columns
+            store_block32(tb, v, true, it.C, it.ldc, it.lane0 + lane_base, it.col0 + c0, nlane, ncol, f32);
+          else        // lanes = columns of C, TMEM columns = output rows
+            store_block32(tb, v, false, it.C, it.ldc, it.col0 + c0, it.lane0 + lane_base, ncol, nlane, f32);
         }
       }
       tc_fence_before();

@@ -1,0 +1,227 @@
+// kernel_tc2.cu — K1b: the CTA-pair (cta_group::2) uKernel executor.
+//
+// Clusters of two CTAs on a TPC execute "pair items": two 128-lane slabs of
+// one problem (the lane operand rows of each CTA can be anywhere) that share
+// the same column range. One tcgen05.mma.cta_group::2 (M = 256, N = n_mma,
+// K = 16) issued by the leader CTA reads each CTA's 128-row lane tile and each
+// CTA's half of the column tile (N/2 rows) from the two shared memories and
+// accumulates 128 x N into each CTA's own TMEM. Per CTA and K block the smem
+// traffic is 16 KiB + N*64 B instead of 16 KiB + N*128 B, which is what lets
+// the dense GEMMs outrun the per-SM operand-delivery limit of K1.
+//
+// Roles (per CTA, both CTAs unless noted):
+//   warp 0      TMA producer: waits its own `empty` slot (released by the
+//               leader's multicast commit), loads its lane slab and its half
+//               of the column tile with cta_group::2 TMA whose completion
+//               bytes land on the LEADER's `full` barrier.
+//   warp 1      (leader only) MMA issuer; commits stages and finished items to
+//               both CTAs with multicast tcgen05.commit.
+//   warps 2..5  epilogue over the CTA's own 128 lanes; releases an
+//               accumulator slot by arriving on the leader's `tempty`.
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+
+#include "epilogue.cuh"
+#include "exec_types.h"
+#include "ptx.cuh"
+
+namespace ftb {
+
+__device__ __forceinline__ TcPair load_pair(const TcPair* __restrict__ work, int w) {
+  TcPair it;
+  const uint4* src = reinterpret_cast<const uint4*>(work + w);
+  uint4* dst = reinterpret_cast<uint4*>(&it);
+#pragma unroll
+  for (int q = 0; q < 4; ++q) dst[q] = __ldg(src + q);
+  return it;
+}
+
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kTcThreads, 1)
+    ftb_tc2_kernel(const TcPair* __restrict__ work, int32_t n_work, TcConfig cfg) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
+                                             ~static_cast<uintptr_t>(1023));
+  const int S = cfg.stages;
+  uint8_t* lane_buf = smem;                                   // S x 16 KiB
+  uint8_t* col_buf = smem + S * kLaneStageBytes;              // S x col_stage_bytes (N/2 rows)
+  float* epi_buf = reinterpret_cast<float*>(col_buf + S * cfg.col_stage_bytes);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(reinterpret_cast<uint8_t*>(epi_buf) + kEpiStageBytes);
+  uint64_t* full = bars;                      // [S]     leader: TMA bytes of both CTAs
+  uint64_t* empty = bars + kMaxStages;        // [S]     both: multicast commit
+  uint64_t* tfull = bars + 2 * kMaxStages;    // [n_acc] both: multicast commit
+  uint64_t* tempty = bars + 3 * kMaxStages;   // [n_acc] leader: 8 epilogue-warp arrivals
+  uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(bars + 4 * kMaxStages);
+
+  const int warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
+  const uint32_t rank = cluster_ctarank();
+  const bool leader = rank == 0;
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < S; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    for (int a = 0; a < cfg.n_acc; ++a) {
+      mbar_init(&tfull[a], 1);
+      mbar_init(&tempty[a], 8);  // 4 epilogue warps x 2 CTAs
+    }
+    fence_barrier_init();
+  }
+  if (warp == 2) tmem_alloc_pair<kTmemCols>(tmem_holder);
+  tc_fence_before();
+  cluster_sync();  // barriers of both CTAs initialised, TMEM allocated on both
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_holder;
+  const int G = gridDim.x >> 1;          // clusters
+  const int cid = blockIdx.x >> 1;       // this cluster
+
+  if (warp == 0) {
+    // ------------------------------------------------------------ producer (both CTAs)
+    if (lane == 0) {
+      uint32_t g = 0;
+      TcPair nxt;
+      if (cid < n_work) nxt = load_pair(work, cid);
+      for (int w = cid; w < n_work; w += G) {
+        const TcPair it = nxt;
+        if (w + G < n_work) nxt = load_pair(work, w + G);
+        const bool lane_mn = it.flags & kFlagLaneMN, col_mn = it.flags & kFlagColMN;
+        const int half = it.n_mma >> 1;
+        const int lane0 = rank ? it.lane0[1] : it.lane0[0];
+        const int colr = it.col0 + static_cast<int>(rank) * half;
+        const uint32_t bytes_cta = kLaneStageBytes + static_cast<uint32_t>(half) * kBlockK * 2;
+        for (int kb = 0; kb < it.num_kb; ++kb, ++g) {
+          const uint32_t s = g % S;
+          const uint32_t round = g / S;
+          mbar_wait(&empty[s], (round & 1) ^ 1);
+          const uint32_t fb = mapa_shared(smem_addr(&full[s]), 0);
+          if (leader) mbar_arrive_expect_tx(&full[s], 2 * bytes_cta);
+          uint8_t* ldst = lane_buf + s * kLaneStageBytes;
+          uint8_t* cdst = col_buf + s * cfg.col_stage_bytes;
+          const int k0 = kb * kBlockK;
+          if (!lane_mn) {
+            tma_load_3d_pair(ldst, &it.maps->lane, fb, k0, lane0, it.batch);
+          } else {
+            tma_load_3d_pair(ldst, &it.maps->lane, fb, lane0, k0, it.batch);
+            tma_load_3d_pair(ldst + 8192, &it.maps->lane, fb, lane0 + 64, k0, it.batch);
+          }
+          if (!col_mn) {
+            int r = 0;
+#pragma unroll 1
+            for (int q = 0; q < 4; ++q) {
+              const int rows = 128 >> q;
+              while (half - r >= rows) {
+                tma_load_3d_pair(cdst + r * 128, &it.maps->col[q], fb, k0, colr + r, it.batch);
+                r += rows;
+              }
+            }
+          } else {
+            for (int c = 0; c < half; c += 64)
+              tma_load_3d_pair(cdst + c * 128, &it.maps->col[0], fb, colr + c, k0, it.batch);
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    // ------------------------------------------------------------ MMA issuer (leader)
+    if (leader && lane == 0) {
+      uint32_t g = 0;
+      uint32_t local = 0;
+      TcPair nxt;
+      if (cid < n_work) nxt = load_pair(work, cid);
+      for (int w = cid; w < n_work; w += G, ++local) {
+        const TcPair it = nxt;
+        if (w + G < n_work) nxt = load_pair(work, w + G);
+        const uint32_t slot = local % cfg.n_acc;
+        const uint32_t use = local / cfg.n_acc;
+        const uint32_t lane_mn = (it.flags & kFlagLaneMN) ? 1u : 0u;
+        const uint32_t col_mn = (it.flags & kFlagColMN) ? 1u : 0u;
+        mbar_wait(&tempty[slot], (use & 1) ^ 1);
+        tc_fence_after();
+        const uint32_t tmem_d = tmem_base + slot * cfg.acc_cols;
+        const uint32_t idesc = idesc_bf16_f32(2 * kLaneRows, static_cast<uint32_t>(it.n_mma), lane_mn, col_mn);
+        for (int kb = 0; kb < it.num_kb; ++kb, ++g) {
+          const uint32_t s = g % S;
+          const uint32_t round = g / S;
+          mbar_wait(&full[s], round & 1);
+          tc_fence_after();
+          const uint32_t la = smem_addr(lane_buf + s * kLaneStageBytes);
+          const uint32_t ca = smem_addr(col_buf + s * cfg.col_stage_bytes);
+#pragma unroll
+          for (int kk = 0; kk < kBlockK / 16; ++kk) {
+            const uint64_t adesc = lane_mn ? umma_desc_sw128(la + kk * 2048, 8192, 1024)
+                                           : umma_desc_sw128(la + kk * 32, 16, 1024);
+            const uint64_t bdesc = col_mn ? umma_desc_sw128(ca + kk * 2048, 8192, 1024)
+                                          : umma_desc_sw128(ca + kk * 32, 16, 1024);
+            tc_mma_f16_pair(tmem_d, adesc, bdesc, idesc, (kb | kk) != 0);
+          }
+          tc_commit_pair_mc(&empty[s]);
+        }
+        tc_commit_pair_mc(&tfull[slot]);
+      }
+    }
+  } else {
+    // ------------------------------------------------------------ epilogue (both CTAs)
+    const int quad = warp & 3;
+    float* tb = epi_buf + quad * (32 * 33);
+    uint32_t local = 0;
+    TcPair nxt;
+    if (cid < n_work) nxt = load_pair(work, cid);
+    for (int w = cid; w < n_work; w += G, ++local) {
+      const TcPair it = nxt;
+      if (w + G < n_work) nxt = load_pair(work, w + G);
+      const uint32_t slot = local % cfg.n_acc;
+      const uint32_t use = local / cfg.n_acc;
+      const bool swap = it.flags & kFlagSwap, f32 = it.flags & kFlagOutF32;
+      const int lane_len = rank ? it.lane_len[1] : it.lane_len[0];
+      const int lane0 = rank ? it.lane0[1] : it.lane0[0];
+      mbar_wait(&tfull[slot], use & 1);
+      tc_fence_after();
+      const int lane_base = quad * 32;
+      if (lane_base < lane_len) {
+        const uint32_t taddr = tmem_base + (static_cast<uint32_t>(lane_base) << 16) + slot * cfg.acc_cols;
+        for (int c0 = 0; c0 < it.col_len; c0 += 32) {
+          uint32_t raw[32];
+          tmem_ld_32x32b_x32(taddr + c0, raw);
+          tmem_ld_wait();
+          float v[32];
+#pragma unroll
+          for (int e = 0; e < 32; ++e) v[e] = __uint_as_float(raw[e]);
+          const int ncol = min(32, it.col_len - c0);
+          const int nlane = min(32, lane_len - lane_base);
+          if (!swap)  // lanes = rows of C, TMEM columns = output columns
+            store_block32(tb, v, true, it.C, it.ldc, lane0 + lane_base, it.col0 + c0, nlane, ncol, f32);
+          else        // lanes = columns of C, TMEM columns = output rows
+            store_block32(tb, v, false, it.C, it.ldc, it.col0 + c0, lane0 + lane_base, ncol, nlane, f32);
+        }
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive_cluster(mapa_shared(smem_addr(&tempty[slot]), 0));
+    }
+  }
+
+  tc_fence_before();
+  cluster_sync();  // no CTA leaves while its peer may still touch its smem / barriers
+  if (warp == 2) {
+    tc_fence_after();
+    tmem_dealloc_pair<kTmemCols>(tmem_base);
+  }
+}
+
+int tc_smem_bytes(const TcConfig& cfg);
+
+cudaError_t launch_tc2(const TcPair* work, int32_t n_work, int32_t n_ctas, TcConfig cfg,
+                       cudaStream_t stream) {
+  static bool configured = false;
+  if (!configured) {
+    cudaError_t e = cudaFuncSetAttribute(ftb_tc2_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 232448);
+    if (e != cudaSuccess) return e;
+    configured = true;
+  }
+  if (n_work == 0) return cudaSuccess;
+  ftb_tc2_kernel<<<n_ctas, kTcThreads, tc_smem_bytes(cfg), stream>>>(work, n_work, cfg);
+  return cudaGetLastError();
+}
+
+}  // namespace ftb

@@ -178,7 +178,7 @@ static std::vector<int64_t> reduce_options(int64_t e, int64_t align) {  // ukern
   return v;
 }
 
-bool tcgen05_legal(const Instance& in, const int64_t* smem) {
+bool tcgen05_legal(const Instance& in, const int64_t* smem, int relax_tau) {
   // B200 extension: the uKernel's output tile must map onto efficient
   // tcgen05 tiles in one of the two orientations: 128 or 256 TMEM lanes
   // (M = 128 per MMA) x 64..256 accumulator columns (MMA N, step 32); a tile
@@ -193,6 +193,13 @@ bool tcgen05_legal(const Instance& in, const int64_t* smem) {
   auto col_ok = [](int64_t t, int64_t E) { return (t % 32 == 0 && t >= 64 && t <= 256) || (t >= E && t <= 256); };
   for (int r = in.ns; r < in.na(); ++r)
     if (smem[r] % 64) return false;
+  if (relax_tau == ai || relax_tau == aj) {
+    // fallback rung: the main-axis tile may take any size <= 256 (it is
+    // padded inside the MMA tile); the other output axis stays strict
+    const int64_t t_tau = relax_tau == ai ? ti : tj, t_o = relax_tau == ai ? tj : ti;
+    const int64_t E_o = relax_tau == ai ? Ej : Ei;
+    return t_tau <= 256 && (lane_ok(t_o, E_o) || col_ok(t_o, E_o));
+  }
   return (lane_ok(ti, Ei) && col_ok(tj, Ej)) || (lane_ok(tj, Ej) && col_ok(ti, Ei));
 }
 
@@ -287,7 +294,7 @@ Cands enumerate_legal(const Instance& in, const Hw& hw, int64_t cap, bool* trunc
   if (hw.legality) {  // B200 extension, applied right after enumeration + cap truncation
     std::vector<int64_t> keep;
     for (size_t i = 0; i < all.size(); ++i)
-      if (tcgen05_legal(in, all.smem_row(i))) keep.push_back(static_cast<int64_t>(i));
+      if (tcgen05_legal(in, all.smem_row(i), hw.relax_tau)) keep.push_back(static_cast<int64_t>(i));
     subset_inplace(all, keep);
   }
   return all;

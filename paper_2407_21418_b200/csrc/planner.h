@@ -44,7 +44,8 @@ struct Instance {
 
 struct Hw {
   int64_t cores, regs, smem, bw_g, bw_s, peak, zeta, active, align;
-  int legality;
+  int legality;       // 0 parity, 1 tcgen05 legality (B200 mode)
+  int relax_tau = -1; // B200 fallback: space axis whose tile only needs t <= 256
   static Hw from_c(const ftb_hw& h);
 };
 
@@ -102,7 +103,7 @@ std::vector<PlanRow> pool_export(const Cands& c, int tau);
 std::vector<std::pair<PlanRow, double>> rank_topk(const Cands& c, int tau, const ftb_coeffs& co,
                                                   int k, bool normalize);
 // B200 legality predicate (extension; parity mode never calls it).
-bool tcgen05_legal(const Instance& in, const int64_t* smem);
+bool tcgen05_legal(const Instance& in, const int64_t* smem, int relax_tau = -1);
 
 }  // namespace plan
 }  // namespace ftb
