@@ -1,0 +1,82 @@
+"""Planner -> lowering -> sm_100a executor, end to end on B200, for every
+BASELINE config family: C0 (fp32 FFMA validation mode, 1e-5), C1/C3 Dense,
+C2 attention BMM (bf16, 2e-2), and the grouped C1 shape set in one launch.
+Reference: the same op in float64 on the device (norm-wise relative error)."""
+
+import pytest
+import torch
+
+from paper_2407_21418_b200.runtime import Planner
+from paper_2407_21418_b200.shapeset import ShapeSet
+from paper_2407_21418_b200.workloads import Shape, c1_shapes
+
+pytestmark = pytest.mark.gpu
+
+
+def rel(c, ref):
+    return ((c.double() - ref).abs().max() / ref.abs().max().clamp_min(1e-30)).item()
+
+
+@pytest.fixture(scope="module")
+def planner():
+    return Planner()
+
+
+@pytest.mark.parametrize("M", [1, 7, 16, 127, 1000, 2116, 4097])
+def test_c3_dense_4096(cuda, planner, M):
+    g = torch.Generator(device=cuda).manual_seed(M)
+    A = (torch.rand(M, 4096, device=cuda, generator=g) * 2 - 1).bfloat16()
+    W = (torch.rand(4096, 4096, device=cuda, generator=g) * 2 - 1).bfloat16()
+    C = planner.dense(A, W, b_layout="nk")
+    torch.cuda.synchronize()
+    assert rel(C, A.double() @ W.double().t()) < 2e-2
+
+
+@pytest.mark.parametrize("M", [1, 2, 53, 64, 127, 509, 512])
+def test_c0_fp32_ffma(cuda, planner, M):
+    g = torch.Generator(device=cuda).manual_seed(M)
+    A = torch.rand(M, 768, device=cuda, generator=g) * 2 - 1
+    B = torch.rand(768, 768, device=cuda, generator=g) * 2 - 1
+    C = planner.dense(A, B, b_layout="kn")
+    torch.cuda.synchronize()
+    assert C.dtype == torch.float32
+    assert rel(C, A.double() @ B.double()) < 1e-5
+
+
+@pytest.mark.parametrize("T", [1, 8, 64, 257, 512])
+def test_c2_bmm_attention(cuda, planner, T):
+    shapes = [Shape("bmm", "scores", 1024, T, T, 64, "nk", ("i", "j")),
+              Shape("bmm", "context", 1024, T, 64, T, "kn", ("i", "k"))]
+    ss = ShapeSet(shapes, planner, device=cuda, seed=T)
+    ss.launch()
+    torch.cuda.synchronize()
+    for i, x in enumerate(ss.bound):
+        assert rel(x.C, ss.reference_outputs(i)) < 2e-2, x.shape
+
+
+def test_c1_grouped_table(cuda, planner):
+    ss = ShapeSet(c1_shapes(n_draws=4, seed=5), planner, device=cuda, seed=1)
+    for x in ss.bound:
+        x.C_store.fill_(float("nan"))
+    ss.launch()
+    torch.cuda.synchronize()
+    for i, x in enumerate(ss.bound):
+        assert not torch.isnan(x.C.float()).any(), x.shape
+        assert rel(x.C, ss.reference_outputs(i)) < 2e-2, x.shape
+
+
+def test_graph_capture_and_replay(cuda, planner):
+    ss = ShapeSet(c1_shapes(n_draws=1, seed=2)[:12], planner, device=cuda, seed=2)
+    s = torch.cuda.Stream(cuda)
+    g = torch.cuda.CUDAGraph()
+    ss.launch(s)
+    torch.cuda.synchronize()
+    with torch.cuda.graph(g, stream=s):
+        ss.launch(s)
+    for x in ss.bound:
+        x.C_store.zero_()
+    with torch.cuda.stream(s):
+        g.replay()
+    torch.cuda.synchronize()
+    for i, x in enumerate(ss.bound):
+        assert rel(x.C, ss.reference_outputs(i)) < 2e-2
