@@ -271,8 +271,8 @@ static void build(ExecImpl& ex, const ftb_gemm_desc* probs, const ftb_program* p
       else
         encode_map(&m.lane, lane_t, lane_rows, d.K, d.batch, lane_ld, lane_bs, 64, 64);
       if (!P.col_mn) {
-        for (int q = 0; q < 4; ++q)
-          encode_map(&m.col[q], col_t, d.K, col_rows, d.batch, col_ld, col_bs, 64, 128u >> q);
+        for (int q = 0; q < kColMaps; ++q)
+          encode_map(&m.col[q], col_t, d.K, col_rows, d.batch, col_ld, col_bs, 64, 256u >> q);
       } else {
         encode_map(&m.col[0], col_t, col_rows, d.K, d.batch, col_ld, col_bs, 64, 64);
       }
@@ -518,7 +518,7 @@ ftb_status ftb_exec_set_trace(ftb_exec* ex, int32_t enable) {
     auto& I = ex->impl;
     if (I.info.kernel != 0) throw ftb::input_error("tracing is only available for the tcgen05 kernel");
     if (enable && !I.d_trace) {
-      const size_t n = static_cast<size_t>(I.info.n_ctas) * ftb::kTraceItems * ftb::kTraceEvents;
+      const size_t n = static_cast<size_t>(I.info.n_ctas) * ftb::kTracePerCta;
       FTB_CUDA(cudaMalloc(&I.d_trace, n * sizeof(unsigned long long)));
       FTB_CUDA(cudaMemset(I.d_trace, 0, n * sizeof(unsigned long long)));
     }
@@ -530,7 +530,7 @@ ftb_status ftb_exec_read_trace(const ftb_exec* ex, uint64_t* out, int64_t cap, i
   return ftb::guarded([&] {
     if (!ex || !n_out) throw ftb::input_error("null argument");
     const auto& I = ex->impl;
-    const int64_t n = I.d_trace ? I.info.n_ctas * ftb::kTraceItems * ftb::kTraceEvents : 0;
+    const int64_t n = I.d_trace ? I.info.n_ctas * ftb::kTracePerCta : 0;
     *n_out = n;
     if (out && n) FTB_CUDA(cudaMemcpy(out, I.d_trace, sizeof(uint64_t) * std::min(cap, n), cudaMemcpyDeviceToHost));
   });

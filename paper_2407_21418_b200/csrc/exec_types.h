@@ -28,12 +28,20 @@ struct DevProblem {
 
 // TMA descriptors of one problem for the tcgen05 kernel (64-B aligned).
 //   lane  : box {64, 128} (K-major) or {64 MN, 64 K} (MN-major)
-//   col[q]: K-major boxes of 128 >> q rows (q = 0..3: 128, 64, 32, 16);
+//   col[q]: K-major boxes of 256 >> q rows (q = 0..4: 256, 128, 64, 32, 16);
 //           MN-major: col[0] = box {64 MN, 64 K}
 struct alignas(64) DevMaps {
   CUtensorMap lane;
-  CUtensorMap col[4];
+  CUtensorMap col[5];
 };
+constexpr int kColMaps = 5;
+
+// Which col[] boxes cover n rows (n multiple of 16, <= 256): bit q set = one
+// box of 256 >> q rows; boxes are placed widest first.
+__host__ __device__ inline uint32_t col_box_mask(int n) {
+  if (n >= 256) return 1u;
+  return (((n >> 7) & 1u) << 1) | (((n >> 6) & 1u) << 2) | (((n >> 5) & 1u) << 3) | (((n >> 4) & 1u) << 4);
+}
 
 // Logical work item (host export format, 8 x int32): an output rectangle of
 // at most 128 lanes x 256 columns of one problem.
@@ -88,6 +96,8 @@ struct TcConfig {
 };
 constexpr int kTraceItems = 16;   // items traced per CTA
 constexpr int kTraceEvents = 6;   // see kernel_tc.cu
+constexpr int kTraceKb = 64;      // K blocks traced per CTA (producer issue, MMA sees data)
+constexpr int kTracePerCta = kTraceItems * kTraceEvents + 2 * kTraceKb;
 
 constexpr int kBlockK = 64;          // one 128-B swizzle atom of bf16 along K
 constexpr int kLaneRows = 128;       // MMA M

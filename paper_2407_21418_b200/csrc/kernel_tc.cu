@@ -45,15 +45,21 @@ __device__ __forceinline__ TcWork load_work(const TcWork* __restrict__ work, int
 //   4 epilogue saw the accumulator  5 epilogue released it
 __device__ __forceinline__ void trace_ev(const TcConfig& cfg, uint32_t local, int ev) {
   if (cfg.trace && local < kTraceItems)
-    cfg.trace[(static_cast<size_t>(blockIdx.x) * kTraceItems + local) * kTraceEvents + ev] = globaltimer();
+    cfg.trace[static_cast<size_t>(blockIdx.x) * kTracePerCta + local * kTraceEvents + ev] = globaltimer();
+}
+// per-K-block events of the first kTraceKb K blocks: 0 producer issued, 1 MMA saw data
+__device__ __forceinline__ void trace_kb(const TcConfig& cfg, uint32_t g, int ev) {
+  if (cfg.trace && g < kTraceKb)
+    cfg.trace[static_cast<size_t>(blockIdx.x) * kTracePerCta + kTraceItems * kTraceEvents + 2 * g + ev] =
+        globaltimer();
 }
 
+template <int S>
 __global__ void __launch_bounds__(kTcThreads, 1)
     ftb_tc_kernel(const TcWork* __restrict__ work, int32_t n_work, TcConfig cfg) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                              ~static_cast<uintptr_t>(1023));
-  const int S = cfg.stages;
   uint8_t* lane_buf = smem;                                   // S x 16 KiB
   uint8_t* col_buf = smem + S * kLaneStageBytes;              // S x col_stage_bytes
   float* epi_buf = reinterpret_cast<float*>(col_buf + S * cfg.col_stage_bytes);  // 4 x 32x33
@@ -88,7 +94,8 @@ __global__ void __launch_bounds__(kTcThreads, 1)
   if (warp == 0) {
     // ------------------------------------------------------------ producer
     if (lane == 0) {
-      uint32_t g = 0;  // global K-block counter (ring position)
+      uint32_t g = 0;
+      uint32_t ps = 0, pphase = 0;  // producer ring slot / phase  // global K-block counter (ring position)
       uint32_t local = 0;
       TcWork nxt;
       if (static_cast<int>(blockIdx.x) < n_work) nxt = load_work(work, blockIdx.x);
@@ -105,10 +112,20 @@ __global__ void __launch_bounds__(kTcThreads, 1)
         }
         const bool lane_mn = it.flags & kFlagLaneMN, col_mn = it.flags & kFlagColMN;
         const uint32_t bytes = kLaneStageBytes + static_cast<uint32_t>(it.n_mma) * kBlockK * 2;
+        const uint32_t cmask = col_box_mask(it.n_mma);
+        int boff[kColMaps];  // smem row offset of each column box (widest first)
+        {
+          int r = 0;
+#pragma unroll
+          for (int q = 0; q < kColMaps; ++q) {
+            boff[q] = r;
+            if (cmask & (1u << q)) r += 256 >> q;
+          }
+        }
         for (int kb = 0; kb < it.num_kb; ++kb, ++g) {
-          const uint32_t s = g % S;
-          const uint32_t round = g / S;
-          mbar_wait(&empty[s], (round & 1) ^ 1);
+          const uint32_t s = ps;
+          mbar_wait(&empty[s], pphase ^ 1);
+          if (++ps == S) { ps = 0; pphase ^= 1; }
           mbar_arrive_expect_tx(&full[s], bytes);
           uint8_t* ldst = lane_buf + s * kLaneStageBytes;
           uint8_t* cdst = col_buf + s * cfg.col_stage_bytes;
@@ -120,21 +137,16 @@ __global__ void __launch_bounds__(kTcThreads, 1)
             tma_load_3d(ldst + 8192, tl, &full[s], it.lane0 + 64, k0, it.batch);
           }
           if (!col_mn) {
-            // widest boxes first: 128, 64, 32, 16 rows
-            int r = 0;
-#pragma unroll 1
-            for (int q = 0; q < 4; ++q) {
-              const int rows = 128 >> q;
-              while (it.n_mma - r >= rows) {
-                tma_load_3d(cdst + r * 128, &it.maps->col[q], &full[s], k0, it.col0 + r, it.batch);
-                r += rows;
-              }
-            }
+#pragma unroll
+            for (int q = 0; q < kColMaps; ++q)
+              if (cmask & (1u << q))
+                tma_load_3d(cdst + boff[q] * 128, &it.maps->col[q], &full[s], k0, it.col0 + boff[q], it.batch);
           } else {
             for (int c = 0; c < it.n_mma; c += 64)
               tma_load_3d(cdst + c * 128, &it.maps->col[0], &full[s], it.col0 + c, k0, it.batch);
           }
           if (kb == 0) trace_ev(cfg, local, 1);
+          trace_kb(cfg, g, 0);
         }
       }
     }
@@ -142,6 +154,7 @@ __global__ void __launch_bounds__(kTcThreads, 1)
     // ------------------------------------------------------------ MMA issuer
     if (lane == 0) {
       uint32_t g = 0;
+      uint32_t ms = 0, mphase = 0;  // MMA ring slot / phase
       uint32_t local = 0;
       TcWork nxt;
       if (static_cast<int>(blockIdx.x) < n_work) nxt = load_work(work, blockIdx.x);
@@ -157,11 +170,12 @@ __global__ void __launch_bounds__(kTcThreads, 1)
         const uint32_t tmem_d = tmem_base + slot * cfg.acc_cols;
         const uint32_t idesc = idesc_bf16_f32(kLaneRows, static_cast<uint32_t>(it.n_mma), lane_mn, col_mn);
         for (int kb = 0; kb < it.num_kb; ++kb, ++g) {
-          const uint32_t s = g % S;
-          const uint32_t round = g / S;
-          mbar_wait(&full[s], round & 1);
+          const uint32_t s = ms;
+          mbar_wait(&full[s], mphase);
+          if (++ms == S) { ms = 0; mphase ^= 1; }
           tc_fence_after();
           if (kb == 0) trace_ev(cfg, local, 2);
+          trace_kb(cfg, g, 1);
           const uint32_t la = smem_addr(lane_buf + s * kLaneStageBytes);
           const uint32_t ca = smem_addr(col_buf + s * cfg.col_stage_bytes);
 #pragma unroll
@@ -232,19 +246,32 @@ int tc_smem_bytes(const TcConfig& cfg) {
          (4 * kMaxStages + 2) * 8;
 }
 
+template <int S>
+static cudaError_t launch_tc_s(const TcWork* work, int32_t n_work, int32_t n_ctas, TcConfig cfg,
+                               cudaStream_t stream) {
+  static bool configured = false;
+  if (!configured) {
+    cudaError_t e = cudaFuncSetAttribute(ftb_tc_kernel<S>, cudaFuncAttributeMaxDynamicSharedMemorySize, 232448);
+    if (e != cudaSuccess) return e;
+    configured = true;
+  }
+  ftb_tc_kernel<S><<<n_ctas, kTcThreads, tc_smem_bytes(cfg), stream>>>(work, n_work, cfg);
+  return cudaGetLastError();
+}
+
 cudaError_t launch_tc(const TcWork* work, int32_t n_work, int32_t n_ctas, TcConfig cfg,
                       cudaStream_t stream) {
-  static int configured = 0;
-  const int smem = tc_smem_bytes(cfg);
-  if (smem > configured) {
-    cudaError_t e = cudaFuncSetAttribute(ftb_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         232448);
-    if (e != cudaSuccess) return e;
-    configured = 232448;
-  }
   if (n_work == 0) return cudaSuccess;
-  ftb_tc_kernel<<<n_ctas, kTcThreads, smem, stream>>>(work, n_work, cfg);
-  return cudaGetLastError();
+  switch (cfg.stages) {
+    case 2: return launch_tc_s<2>(work, n_work, n_ctas, cfg, stream);
+    case 3: return launch_tc_s<3>(work, n_work, n_ctas, cfg, stream);
+    case 4: return launch_tc_s<4>(work, n_work, n_ctas, cfg, stream);
+    case 5: return launch_tc_s<5>(work, n_work, n_ctas, cfg, stream);
+    case 6: return launch_tc_s<6>(work, n_work, n_ctas, cfg, stream);
+    case 7: return launch_tc_s<7>(work, n_work, n_ctas, cfg, stream);
+    case 8: return launch_tc_s<8>(work, n_work, n_ctas, cfg, stream);
+    default: return cudaErrorInvalidValue;
+  }
 }
 
 }  // namespace ftb

@@ -36,12 +36,12 @@ __device__ __forceinline__ TcPair load_pair(const TcPair* __restrict__ work, int
   return it;
 }
 
+template <int S>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kTcThreads, 1)
     ftb_tc2_kernel(const TcPair* __restrict__ work, int32_t n_work, TcConfig cfg) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                              ~static_cast<uintptr_t>(1023));
-  const int S = cfg.stages;
   uint8_t* lane_buf = smem;                                   // S x 16 KiB
   uint8_t* col_buf = smem + S * kLaneStageBytes;              // S x col_stage_bytes (N/2 rows)
   float* epi_buf = reinterpret_cast<float*>(col_buf + S * cfg.col_stage_bytes);
@@ -80,6 +80,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kTcThreads, 1)
     // ------------------------------------------------------------ producer (both CTAs)
     if (lane == 0) {
       uint32_t g = 0;
+      uint32_t ps = 0, pphase = 0;  // producer ring slot / phase
       TcPair nxt;
       if (cid < n_work) nxt = load_pair(work, cid);
       for (int w = cid; w < n_work; w += G) {
@@ -90,10 +91,20 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kTcThreads, 1)
         const int lane0 = rank ? it.lane0[1] : it.lane0[0];
         const int colr = it.col0 + static_cast<int>(rank) * half;
         const uint32_t bytes_cta = kLaneStageBytes + static_cast<uint32_t>(half) * kBlockK * 2;
+        const uint32_t cmask = col_box_mask(half);
+        int boff[kColMaps];  // smem row offset of each column box (widest first)
+        {
+          int r = 0;
+#pragma unroll
+          for (int q = 0; q < kColMaps; ++q) {
+            boff[q] = r;
+            if (cmask & (1u << q)) r += 256 >> q;
+          }
+        }
         for (int kb = 0; kb < it.num_kb; ++kb, ++g) {
-          const uint32_t s = g % S;
-          const uint32_t round = g / S;
-          mbar_wait(&empty[s], (round & 1) ^ 1);
+          const uint32_t s = ps;
+          mbar_wait(&empty[s], pphase ^ 1);
+          if (++ps == S) { ps = 0; pphase ^= 1; }
           const uint32_t fb = mapa_shared(smem_addr(&full[s]), 0);
           if (leader) mbar_arrive_expect_tx(&full[s], 2 * bytes_cta);
           uint8_t* ldst = lane_buf + s * kLaneStageBytes;
@@ -106,15 +117,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kTcThreads, 1)
             tma_load_3d_pair(ldst + 8192, &it.maps->lane, fb, lane0 + 64, k0, it.batch);
           }
           if (!col_mn) {
-            int r = 0;
-#pragma unroll 1
-            for (int q = 0; q < 4; ++q) {
-              const int rows = 128 >> q;
-              while (half - r >= rows) {
-                tma_load_3d_pair(cdst + r * 128, &it.maps->col[q], fb, k0, colr + r, it.batch);
-                r += rows;
-              }
-            }
+#pragma unroll
+            for (int q = 0; q < kColMaps; ++q)
+              if (cmask & (1u << q))
+                tma_load_3d_pair(cdst + boff[q] * 128, &it.maps->col[q], fb, k0, colr + boff[q], it.batch);
           } else {
             for (int c = 0; c < half; c += 64)
               tma_load_3d_pair(cdst + c * 128, &it.maps->col[0], fb, colr + c, k0, it.batch);
@@ -126,6 +132,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kTcThreads, 1)
     // ------------------------------------------------------------ MMA issuer (leader)
     if (leader && lane == 0) {
       uint32_t g = 0;
+      uint32_t ms = 0, mphase = 0;  // MMA ring slot / phase
       uint32_t local = 0;
       TcPair nxt;
       if (cid < n_work) nxt = load_pair(work, cid);
@@ -141,9 +148,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kTcThreads, 1)
         const uint32_t tmem_d = tmem_base + slot * cfg.acc_cols;
         const uint32_t idesc = idesc_bf16_f32(2 * kLaneRows, static_cast<uint32_t>(it.n_mma), lane_mn, col_mn);
         for (int kb = 0; kb < it.num_kb; ++kb, ++g) {
-          const uint32_t s = g % S;
-          const uint32_t round = g / S;
-          mbar_wait(&full[s], round & 1);
+          const uint32_t s = ms;
+          mbar_wait(&full[s], mphase);
+          if (++ms == S) { ms = 0; mphase ^= 1; }
           tc_fence_after();
           const uint32_t la = smem_addr(lane_buf + s * kLaneStageBytes);
           const uint32_t ca = smem_addr(col_buf + s * cfg.col_stage_bytes);
@@ -211,17 +218,32 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kTcThreads, 1)
 
 int tc_smem_bytes(const TcConfig& cfg);
 
-cudaError_t launch_tc2(const TcPair* work, int32_t n_work, int32_t n_ctas, TcConfig cfg,
-                       cudaStream_t stream) {
+template <int S>
+static cudaError_t launch_tc2_s(const TcPair* work, int32_t n_work, int32_t n_ctas, TcConfig cfg,
+                                cudaStream_t stream) {
   static bool configured = false;
   if (!configured) {
-    cudaError_t e = cudaFuncSetAttribute(ftb_tc2_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 232448);
+    cudaError_t e = cudaFuncSetAttribute(ftb_tc2_kernel<S>, cudaFuncAttributeMaxDynamicSharedMemorySize, 232448);
     if (e != cudaSuccess) return e;
     configured = true;
   }
-  if (n_work == 0) return cudaSuccess;
-  ftb_tc2_kernel<<<n_ctas, kTcThreads, tc_smem_bytes(cfg), stream>>>(work, n_work, cfg);
+  ftb_tc2_kernel<S><<<n_ctas, kTcThreads, tc_smem_bytes(cfg), stream>>>(work, n_work, cfg);
   return cudaGetLastError();
+}
+
+cudaError_t launch_tc2(const TcPair* work, int32_t n_work, int32_t n_ctas, TcConfig cfg,
+                       cudaStream_t stream) {
+  if (n_work == 0) return cudaSuccess;
+  switch (cfg.stages) {
+    case 2: return launch_tc2_s<2>(work, n_work, n_ctas, cfg, stream);
+    case 3: return launch_tc2_s<3>(work, n_work, n_ctas, cfg, stream);
+    case 4: return launch_tc2_s<4>(work, n_work, n_ctas, cfg, stream);
+    case 5: return launch_tc2_s<5>(work, n_work, n_ctas, cfg, stream);
+    case 6: return launch_tc2_s<6>(work, n_work, n_ctas, cfg, stream);
+    case 7: return launch_tc2_s<7>(work, n_work, n_ctas, cfg, stream);
+    case 8: return launch_tc2_s<8>(work, n_work, n_ctas, cfg, stream);
+    default: return cudaErrorInvalidValue;
+  }
 }
 
 }  // namespace ftb

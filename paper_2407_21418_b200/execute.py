@@ -181,7 +181,8 @@ class Executable:
         _lib.check(_lib.lib().ftb_exec_set_trace(self._h, 1 if enable else 0))
 
     def read_trace(self):
-        """[n_ctas, 16 items, 6 events] of %globaltimer ns (0 = not reached)."""
+        """(items [n_ctas, 16, 6], kblocks [n_ctas, 64, 2]) of %globaltimer ns
+        (0 = not reached); see include/ftb.h ftb_exec_set_trace."""
         import numpy as np
 
         L = _lib.lib()
@@ -189,7 +190,9 @@ class Executable:
         _lib.check(L.ftb_exec_read_trace(self._h, None, 0, C.byref(n)))
         out = np.zeros(n.value, dtype=np.uint64)
         _lib.check(L.ftb_exec_read_trace(self._h, out.ctypes.data_as(C.POINTER(C.c_uint64)), n.value, C.byref(n)))
-        return out.reshape(-1, 16, 6)
+        per = 16 * 6 + 2 * 64
+        out = out.reshape(-1, per)
+        return out[:, : 16 * 6].reshape(-1, 16, 6), out[:, 16 * 6:].reshape(-1, 64, 2)
 
     def table(self):
         """The lowered work items as an int32 numpy array [n_work, 8]."""
