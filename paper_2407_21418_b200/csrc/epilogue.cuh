@@ -2,6 +2,7 @@
 // stores (16-B vectorised when the destination is aligned and the segment is
 // full, element-predicated on ragged uKernel edges) and %globaltimer.
 #pragma once
+#include <cuda.h>
 #include <cuda_bf16.h>
 #include <cstdint>
 
@@ -113,4 +114,48 @@ __device__ __forceinline__ unsigned long long globaltimer() {
   return t;
 }
 
+}  // namespace ftb
+
+namespace ftb {
+// ---------------------------------------------------------------- TMA store epilogue
+__device__ __forceinline__ void tma_store_3d(const CUtensorMap* m, uint32_t src, int32_t c0, int32_t c1,
+                                             int32_t c2) {
+  asm volatile("cp.async.bulk.tensor.3d.global.shared::cta.bulk_group [%0, {%2, %3, %4}], [%1];" ::"l"(
+                   reinterpret_cast<uint64_t>(m)),
+               "r"(src), "r"(c0), "r"(c1), "r"(c2)
+               : "memory");
+}
+__device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void bulk_wait_read() {
+  asm volatile("cp.async.bulk.wait_group.read %0;" ::"n"(N) : "memory");
+}
+__device__ __forceinline__ void bulk_wait_all() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
+__device__ __forceinline__ void fence_async_smem() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
+
+// Write a warp's 32 x 32 fp32 accumulator block as bf16 into a TMA store box
+// (32 C rows x 64 B, SWIZZLE_64B: 16-B chunk index ^= row bits [1,3)); the box
+// must be 512-B aligned. lane_is_row: lane l holds C row l (normal
+// orientation); otherwise lane l holds C column l and register e is C row e.
+__device__ __forceinline__ void stage_box_bf16(uint8_t* box, const uint32_t (&r)[32], bool lane_is_row) {
+  const int l = threadIdx.x & 31;
+  if (lane_is_row) {
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      uint4 pk;
+      uint32_t* pw = reinterpret_cast<uint32_t*>(&pk);
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        __nv_bfloat162 h = __floats2bfloat162_rn(__uint_as_float(r[q * 8 + 2 * e]), __uint_as_float(r[q * 8 + 2 * e + 1]));
+        pw[e] = *reinterpret_cast<uint32_t*>(&h);
+      }
+      *reinterpret_cast<uint4*>(box + l * 64 + ((q ^ ((l >> 1) & 3)) * 16)) = pk;
+    }
+  } else {
+#pragma unroll
+    for (int e = 0; e < 32; ++e)
+      *reinterpret_cast<__nv_bfloat16*>(box + e * 64 + (((l >> 3) ^ ((e >> 1) & 3)) * 16) + (l & 7) * 2) =
+          __float2bfloat16_rn(__uint_as_float(r[e]));
+  }
+}
 }  // namespace ftb

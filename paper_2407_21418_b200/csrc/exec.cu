@@ -78,6 +78,29 @@ void encode_map(CUtensorMap* m, const void* base, int64_t inner, int64_t rows, i
   if (r != CUDA_SUCCESS) throw cuda_error("cuTensorMapEncodeTiled failed: " + std::to_string(r));
 }
 
+// C store map for the TMA-store epilogue (bf16 outputs): dims {N, M, batch},
+// box {32, 32}, 64-B swizzle. Returns false (no TMA stores for this problem)
+// for fp32 outputs or when C violates TMA's 16-byte alignment rules. Measured
+// on B200 (tests/test_exec_gpu.py::test_dense_strided_output_untouched_padding):
+// stores clip the inner dimension at 16-byte granularity, so a row length N
+// that is not a multiple of 8 bf16 would clobber up to 7 elements past the
+// tensor edge — such problems keep the predicated st.global epilogue.
+bool encode_out_map(CUtensorMap* m, const ftb_gemm_desc& d) {
+  if (d.out_dtype != FTB_DT_BF16) return false;
+  if ((d.N * 2) % 16) return false;
+  if (reinterpret_cast<uintptr_t>(d.C) % 16 || (d.ldc * 2) % 16) return false;
+  const int64_t bs = d.batch > 1 ? d.c_batch_stride : d.M * d.ldc;
+  if ((bs * 2) % 16) return false;
+  cuuint64_t dims[3] = {static_cast<cuuint64_t>(d.N), static_cast<cuuint64_t>(d.M), static_cast<cuuint64_t>(d.batch)};
+  cuuint64_t strides[2] = {static_cast<cuuint64_t>(d.ldc * 2), static_cast<cuuint64_t>(bs * 2)};
+  cuuint32_t box[3] = {32, 32, 1};
+  cuuint32_t estr[3] = {1, 1, 1};
+  CUresult r = get_encode()(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, d.C, dims, strides, box, estr,
+                            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_64B,
+                            CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS;
+}
+
 struct Region {
   int64_t lo[3], hi[3];  // per space axis (dense uses 2)
 };
@@ -174,6 +197,7 @@ struct ExecImpl {
   DevProblem* d_problems = nullptr;
   DevWork* d_work = nullptr;
   DevMaps* d_maps = nullptr;
+  std::vector<uint8_t> tma_out;       // per problem: C store map usable
   TcWork* d_tcwork = nullptr;
   TcPair* d_tcpairs = nullptr;
   unsigned long long* d_trace = nullptr;
@@ -276,6 +300,7 @@ static void build(ExecImpl& ex, const ftb_gemm_desc* probs, const ftb_program* p
       } else {
         encode_map(&m.col[0], col_t, col_rows, d.K, d.batch, col_ld, col_bs, 64, 64);
       }
+      ex.tma_out.push_back(encode_out_map(&m.out, d) ? 1 : 0);
       ex.maps.push_back(m);
     }
     ex.problems.push_back(P);
@@ -350,9 +375,12 @@ static void upload(ExecImpl& I) {
     return static_cast<void*>(static_cast<char*>(P.C) + static_cast<int64_t>(batch) * P.c_bs * esz);
   };
   // CTA pairs: logical items of one problem/batch with the same column range
-  // share the column operand; group them (in cost order) two by two.
+  // share the column operand; group them (in cost order) two by two. Off by
+  // default: measured on B200 the pair kernel loses to the single-CTA kernel
+  // with TMA-store epilogues on every C1 shape (profiles/r1b_*); FTB_PAIR=1
+  // enables it.
   const char* env = std::getenv("FTB_PAIR");
-  const bool pairing = !(env && env[0] == '0');
+  const bool pairing = env && env[0] == '1';
   std::vector<int8_t> paired(I.work.size(), 0);
   std::vector<TcPair> pairs;
   if (pairing) {
@@ -387,6 +415,16 @@ static void upload(ExecImpl& I) {
       open.erase(it);
     }
   }
+  // TMA stores write whole 32 x 32 boxes: legal for a rectangle whose extents
+  // are multiples of 32 or that ends at the tensor edge (the hardware clips).
+  const char* env_ts = std::getenv("FTB_TMA_STORE");
+  const bool tma_store_on = !(env_ts && env_ts[0] == '0');
+  auto tma_ok = [&](const DevWork& w) {
+    const DevProblem& P = I.problems[w.problem];
+    const int32_t lane_ext = P.swap ? P.N : P.M, col_ext = P.swap ? P.M : P.N;
+    return tma_store_on && I.tma_out[w.problem] && (w.lane_len % 32 == 0 || w.lane0 + w.lane_len == lane_ext) &&
+           (w.col_len % 32 == 0 || w.col0 + w.col_len == col_ext);
+  };
   std::vector<TcWork> tw;
   int max_n = 16;
   for (size_t i = 0; i < I.work.size(); ++i) {
@@ -405,7 +443,7 @@ static void upload(ExecImpl& I) {
     t.n_mma = w.n_mma;
     t.num_kb = P.num_kb;
     t.batch = w.batch;
-    t.flags = flags_of(P);
+    t.flags = flags_of(P) | (tma_ok(w) ? kFlagTmaStore : 0u);
     max_n = std::max(max_n, w.n_mma);
     tw.push_back(t);
   }

@@ -30,9 +30,12 @@ struct DevProblem {
 //   lane  : box {64, 128} (K-major) or {64 MN, 64 K} (MN-major)
 //   col[q]: K-major boxes of 256 >> q rows (q = 0..4: 256, 128, 64, 32, 16);
 //           MN-major: col[0] = box {64 MN, 64 K}
+//   out   : C store map (bf16 outputs), box {32 cols, 32 rows}, 64-B swizzle;
+//           TMA clips stores at the tensor edge
 struct alignas(64) DevMaps {
   CUtensorMap lane;
   CUtensorMap col[5];
+  CUtensorMap out;
 };
 constexpr int kColMaps = 5;
 
@@ -58,7 +61,10 @@ struct alignas(16) DevWork {
 
 // Self-contained tcgen05 work item (64 B): everything a role needs without a
 // dependent load of the problem record.
-enum : uint32_t { kFlagSwap = 1u, kFlagLaneMN = 2u, kFlagColMN = 4u, kFlagOutF32 = 8u };
+//   kFlagTmaStore: the item's rectangle is whole 32 x 32 store boxes or ends
+//   at the tensor edge, so the epilogue may store through TMA (clipped by the
+//   hardware) instead of predicated st.global.
+enum : uint32_t { kFlagSwap = 1u, kFlagLaneMN = 2u, kFlagColMN = 4u, kFlagOutF32 = 8u, kFlagTmaStore = 16u };
 struct alignas(64) TcWork {
   const DevMaps* maps;
   void* C;            // element 0 of this batch entry's output matrix
@@ -106,7 +112,8 @@ constexpr int kMaxStages = 8;
 constexpr int kLaneStageBytes = kLaneRows * kBlockK * 2;   // 16 KiB
 constexpr int kTmemCols = 512;
 constexpr int kTcThreads = 192;                            // 6 warps
-constexpr int kEpiStageBytes = 4 * 32 * 33 * 4;            // per-warp 32x33 fp32 transpose tiles
+constexpr int kEpiBoxBytes = 4 * 2 * 2048;                // per epilogue warp: two 2 KiB bf16 TMA store boxes
+constexpr int kEpiStageBytes = kEpiBoxBytes + 4 * 32 * 33 * 4;  // + per-warp 32x33 fp32 transpose tiles
 constexpr int kTcSmemBudget = 232448 - 1024;               // max dynamic smem minus align slack
 
 }  // namespace ftb

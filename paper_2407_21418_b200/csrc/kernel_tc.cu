@@ -195,8 +195,9 @@ __global__ void __launch_bounds__(kTcThreads, 1)
   } else {
     // ------------------------------------------------------------ epilogue
     const int quad = warp & 3;  // TMEM lane quadrant this warp may access
-    float* tb = epi_buf + quad * (32 * 33);
-    uint32_t local = 0;
+    float* tb = epi_buf + kEpiBoxBytes / 4 + quad * (32 * 33);
+    uint8_t* boxes = reinterpret_cast<uint8_t*>(epi_buf) + quad * 4096;  // two 2 KiB TMA store boxes
+    uint32_t local = 0, nbox = 0;
     TcWork nxt;
     if (static_cast<int>(blockIdx.x) < n_work) nxt = load_work(work, blockIdx.x);
     for (int w = blockIdx.x; w < n_work; w += G, ++local) {
@@ -205,6 +206,7 @@ __global__ void __launch_bounds__(kTcThreads, 1)
       const uint32_t slot = local % cfg.n_acc;
       const uint32_t use = local / cfg.n_acc;
       const bool swap = it.flags & kFlagSwap, f32 = it.flags & kFlagOutF32;
+      const bool tma = it.flags & kFlagTmaStore;
       mbar_wait(&tfull[slot], use & 1);
       tc_fence_after();
       if (quad == 0 && lane == 0) trace_ev(cfg, local, 4);
@@ -215,6 +217,22 @@ __global__ void __launch_bounds__(kTcThreads, 1)
           uint32_t raw[32];
           tmem_ld_32x32b_x32(taddr + c0, raw);
           tmem_ld_wait();
+          if (tma) {
+            // bf16 box -> swizzled smem -> one TMA store (clipped at the tensor edge)
+            uint8_t* box = boxes + (nbox & 1) * 2048;
+            if (lane == 0) bulk_wait_read<1>();  // the store that last used this box has read it
+            __syncwarp();
+            stage_box_bf16(box, raw, !swap);
+            fence_async_smem();
+            __syncwarp();
+            if (lane == 0) {
+              if (!swap) tma_store_3d(&it.maps->out, smem_addr(box), it.col0 + c0, it.lane0 + lane_base, it.batch);
+              else tma_store_3d(&it.maps->out, smem_addr(box), it.lane0 + lane_base, it.col0 + c0, it.batch);
+              bulk_commit();
+            }
+            ++nbox;
+            continue;
+          }
           float v[32];
 #pragma unroll
           for (int e = 0; e < 32; ++e) v[e] = __uint_as_float(raw[e]);
@@ -231,6 +249,8 @@ __global__ void __launch_bounds__(kTcThreads, 1)
       if (lane == 0) mbar_arrive(&tempty[slot]);
       if (quad == 0 && lane == 0) trace_ev(cfg, local, 5);
     }
+    if (lane == 0) bulk_wait_all();  // output stores complete before the CTA retires
+    __syncwarp();
   }
 
   tc_fence_before();

@@ -53,6 +53,43 @@ def test_dense_bf16(cuda, case, b_layout, orientation):
     assert _rel(Cout, ref) < BF16_TOL
 
 
+@pytest.mark.parametrize("case", DENSE_CASES, ids=lambda c: f"M{c[0]}N{c[1]}K{c[2]}")
+@pytest.mark.parametrize("b_layout", ["kn", "nk"])
+@pytest.mark.parametrize("mode", ["pair", "no_tma_store"])
+def test_dense_bf16_kernel_modes(cuda, case, b_layout, mode, monkeypatch):
+    """The CTA-pair kernel (FTB_PAIR=1) and the predicated st.global epilogue
+    (FTB_TMA_STORE=0) against the same reference as the default path."""
+    if mode == "pair":
+        monkeypatch.setenv("FTB_PAIR", "1")
+    else:
+        monkeypatch.setenv("FTB_TMA_STORE", "0")
+    M, N, K, tau, parts = case
+    A, B, ref = _dense(M, N, K, b_layout, torch.bfloat16, cuda, seed=5)
+    Cout = torch.full((M, N), float("nan"), dtype=torch.bfloat16, device=cuda)
+    ex = Executable([gemm_desc(A, B, Cout, b_layout)], [program_struct(2, tau, parts)])
+    ex.launch()
+    torch.cuda.synchronize()
+    assert not torch.isnan(Cout.float()).any(), "uncovered output elements"
+    assert _rel(Cout, ref) < BF16_TOL
+
+
+@pytest.mark.parametrize("orientation", [0, 1])
+@pytest.mark.parametrize("N", [100, 104, 99])
+def test_dense_strided_output_untouched_padding(cuda, orientation, N):
+    """C as a view of a wider buffer: nothing may be written past the tensor
+    edge (N) — TMA-store boxes clip at 16 B, so N % 8 != 0 takes the
+    predicated epilogue."""
+    M, K = 200, 128
+    A, B, ref = _dense(M, N, K, "nk", torch.bfloat16, cuda, seed=7)
+    store = torch.full((M, 136), float("nan"), dtype=torch.bfloat16, device=cuda)
+    Cout = store[:, :N]
+    ex = Executable([gemm_desc(A, B, Cout, "nk", orientation)], [program_struct(2, 0, [((1, 1), (200, N, 64), 1)])])
+    ex.launch()
+    torch.cuda.synchronize()
+    assert torch.isnan(store[:, N:].float()).all(), "store wrote past the tensor edge"
+    assert _rel(Cout, ref) < BF16_TOL
+
+
 @pytest.mark.parametrize("b_layout", ["kn", "nk"])
 def test_dense_f32_out(cuda, b_layout):
     M, N, K = 130, 384, 192
