@@ -112,8 +112,9 @@ constexpr int kMaxStages = 8;
 constexpr int kLaneStageBytes = kLaneRows * kBlockK * 2;   // 16 KiB
 constexpr int kTmemCols = 512;
 constexpr int kTcThreads = 192;                            // 6 warps
-constexpr int kEpiBoxBytes = 4 * 2 * 2048;                // per epilogue warp: two 2 KiB bf16 TMA store boxes
-constexpr int kEpiStageBytes = kEpiBoxBytes + 4 * 32 * 33 * 4;  // + per-warp 32x33 fp32 transpose tiles
+constexpr int kEpiWarpBytes = 8192;   // per epilogue warp: four 2 KiB bf16 TMA store boxes, or (aliased)
+                                       // the 32x33 fp32 transpose tile of the predicated path
+constexpr int kEpiStageBytes = 4 * kEpiWarpBytes;
 constexpr int kTcSmemBudget = 232448 - 1024;               // max dynamic smem minus align slack
 
 }  // namespace ftb

@@ -195,9 +195,11 @@ __global__ void __launch_bounds__(kTcThreads, 1)
   } else {
     // ------------------------------------------------------------ epilogue
     const int quad = warp & 3;  // TMEM lane quadrant this warp may access
-    float* tb = epi_buf + kEpiBoxBytes / 4 + quad * (32 * 33);
-    uint8_t* boxes = reinterpret_cast<uint8_t*>(epi_buf) + quad * 4096;  // two 2 KiB TMA store boxes
-    uint32_t local = 0, nbox = 0;
+    // per-warp 8 KiB staging region: four 2 KiB TMA store boxes (two groups of
+    // two), or — for predicated items — the 32x33 fp32 transpose tile (aliased)
+    uint8_t* region = reinterpret_cast<uint8_t*>(epi_buf) + quad * kEpiWarpBytes;
+    float* tb = reinterpret_cast<float*>(region);
+    uint32_t local = 0, ngrp = 0;
     TcWork nxt;
     if (static_cast<int>(blockIdx.x) < n_work) nxt = load_work(work, blockIdx.x);
     for (int w = blockIdx.x; w < n_work; w += G, ++local) {
@@ -211,42 +213,68 @@ __global__ void __launch_bounds__(kTcThreads, 1)
       tc_fence_after();
       if (quad == 0 && lane == 0) trace_ev(cfg, local, 4);
       const int lane_base = quad * 32;
+      bool released = false;
       if (lane_base < it.lane_len) {
         const uint32_t taddr = tmem_base + (static_cast<uint32_t>(lane_base) << 16) + slot * cfg.acc_cols;
-        for (int c0 = 0; c0 < it.col_len; c0 += 32) {
-          uint32_t raw[32];
-          tmem_ld_32x32b_x32(taddr + c0, raw);
-          tmem_ld_wait();
-          if (tma) {
-            // bf16 box -> swizzled smem -> one TMA store (clipped at the tensor edge)
-            uint8_t* box = boxes + (nbox & 1) * 2048;
-            if (lane == 0) bulk_wait_read<1>();  // the store that last used this box has read it
+        if (tma) {
+          // groups of two 32-column chunks: both tcgen05.ld in flight, one
+          // proxy fence and one bulk group per pair of TMA stores
+          for (int c0 = 0; c0 < it.col_len; c0 += 64) {
+            const bool two = c0 + 32 < it.col_len;
+            uint32_t ra[32], rb[32];
+            tmem_ld_32x32b_x32(taddr + c0, ra);
+            if (two) tmem_ld_32x32b_x32(taddr + c0 + 32, rb);
+            tmem_ld_wait();
+            if (c0 + 64 >= it.col_len) {  // last TMEM read of the item: hand the slot back now
+              tc_fence_before();
+              __syncwarp();
+              if (lane == 0) mbar_arrive(&tempty[slot]);
+              released = true;
+            }
+            uint8_t* box = region + (ngrp & 1) * 4096;
+            if (lane == 0) bulk_wait_read<1>();  // the group that last used these boxes has read them
             __syncwarp();
-            stage_box_bf16(box, raw, !swap);
+            stage_box_bf16(box, ra, !swap);
+            if (two) stage_box_bf16(box + 2048, rb, !swap);
             fence_async_smem();
             __syncwarp();
             if (lane == 0) {
-              if (!swap) tma_store_3d(&it.maps->out, smem_addr(box), it.col0 + c0, it.lane0 + lane_base, it.batch);
-              else tma_store_3d(&it.maps->out, smem_addr(box), it.lane0 + lane_base, it.col0 + c0, it.batch);
+              const int l0 = it.lane0 + lane_base, k0 = it.col0 + c0;
+              if (!swap) {
+                tma_store_3d(&it.maps->out, smem_addr(box), k0, l0, it.batch);
+                if (two) tma_store_3d(&it.maps->out, smem_addr(box + 2048), k0 + 32, l0, it.batch);
+              } else {
+                tma_store_3d(&it.maps->out, smem_addr(box), l0, k0, it.batch);
+                if (two) tma_store_3d(&it.maps->out, smem_addr(box + 2048), l0, k0 + 32, it.batch);
+              }
               bulk_commit();
             }
-            ++nbox;
-            continue;
+            ++ngrp;
           }
-          float v[32];
+        } else {
+          if (lane == 0) bulk_wait_read<0>();  // the transpose tile aliases this warp's store boxes
+          __syncwarp();
+          for (int c0 = 0; c0 < it.col_len; c0 += 32) {
+            uint32_t raw[32];
+            tmem_ld_32x32b_x32(taddr + c0, raw);
+            tmem_ld_wait();
+            float v[32];
 #pragma unroll
-          for (int e = 0; e < 32; ++e) v[e] = __uint_as_float(raw[e]);
-          const int ncol = min(32, it.col_len - c0);
-          const int nlane = min(32, it.lane_len - lane_base);
-          if (!swap)  // lanes = rows of C, TMEM columns = output columns
-            store_block32(tb, v, true, it.C, it.ldc, it.lane0 + lane_base, it.col0 + c0, nlane, ncol, f32);
-          else        // lanes = columns of C, TMEM columns = output rows
-            store_block32(tb, v, false, it.C, it.ldc, it.col0 + c0, it.lane0 + lane_base, ncol, nlane, f32);
+            for (int e = 0; e < 32; ++e) v[e] = __uint_as_float(raw[e]);
+            const int ncol = min(32, it.col_len - c0);
+            const int nlane = min(32, it.lane_len - lane_base);
+            if (!swap)  // lanes = rows of C, TMEM columns = output columns
+              store_block32(tb, v, true, it.C, it.ldc, it.lane0 + lane_base, it.col0 + c0, nlane, ncol, f32);
+            else        // lanes = columns of C, TMEM columns = output rows
+              store_block32(tb, v, false, it.C, it.ldc, it.col0 + c0, it.lane0 + lane_base, ncol, nlane, f32);
+          }
         }
       }
-      tc_fence_before();
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&tempty[slot]);
+      if (!released) {
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&tempty[slot]);
+      }
       if (quad == 0 && lane == 0) trace_ev(cfg, local, 5);
     }
     if (lane == 0) bulk_wait_all();  // output stores complete before the CTA retires

@@ -170,7 +170,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kTcThreads, 1)
   } else {
     // ------------------------------------------------------------ epilogue (both CTAs)
     const int quad = warp & 3;
-    float* tb = epi_buf + kEpiBoxBytes / 4 + quad * (32 * 33);
+    float* tb = epi_buf + quad * (kEpiWarpBytes / 4);
     uint32_t local = 0;
     TcPair nxt;
     if (cid < n_work) nxt = load_pair(work, cid);

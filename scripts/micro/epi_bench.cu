@@ -15,7 +15,7 @@ struct Maps { CUtensorMap a; CUtensorMap b; CUtensorMap c; };
 
 template <int PAIR>
 __global__ void __launch_bounds__(192, 1) epi_kernel(const __grid_constant__ Maps maps, int items, int KB, int S,
-                                                     int N, unsigned long long* out, int epi, __nv_bfloat16* C) {
+                                                     int N, unsigned long long* out, int epi, __nv_bfloat16* C, int dbg) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   const int b_rows = PAIR ? N / 2 : N;
@@ -83,18 +83,23 @@ __global__ void __launch_bounds__(192, 1) epi_kernel(const __grid_constant__ Map
       if (PAIR) tc_commit_pair_mc(&tfull[slot]); else tc_commit(&tfull[slot]);
     }
   } else if (warp >= 2) {
+    unsigned long long t_ld = 0, t_wait = 0, t_all0 = clock64(), n_chunk = 0, t_tf = 0;
     const int quad = warp & 3;
     for (int item = 0; item < items; ++item) {
       const int slot = item & 1, use = item >> 1;
+      unsigned long long tw0 = clock64();
       mbar_wait(&tfull[slot], use & 1);
+      t_tf += clock64() - tw0;
       tc_fence_after();
       if (epi) {
         const uint32_t taddr = tmem + ((quad * 32) << 16) + slot * 256;
         const int row = blockIdx.x * 128 + quad * 32 + lane;
         for (int c0 = 0; c0 < N; c0 += 32) {
           uint32_t r[32];
+          unsigned long long tl0 = clock64();
           tmem_ld_32x32b_x32(taddr + c0, r);
           tmem_ld_wait();
+          t_ld += clock64() - tl0; ++n_chunk;
           if (epi == 1) {
             uint4* dst = reinterpret_cast<uint4*>(C + (size_t)row * 256 + c0);
 #pragma unroll
@@ -111,8 +116,10 @@ __global__ void __launch_bounds__(192, 1) epi_kernel(const __grid_constant__ Map
             // stage 32x32 bf16 (64-B rows, 64-B swizzle) and TMA-store it
             const int buf = (c0 >> 5) & 1;
             uint8_t* stg = epi_smem + (quad * 2 + buf) * 2048;
+            unsigned long long ta = clock64();
             if (lane == 0) asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
             __syncwarp();
+            t_wait += clock64() - ta;
 #pragma unroll
             for (int q = 0; q < 4; ++q) {
               uint4 pk; uint32_t* pw = reinterpret_cast<uint32_t*>(&pk);
@@ -141,6 +148,9 @@ __global__ void __launch_bounds__(192, 1) epi_kernel(const __grid_constant__ Map
         else mbar_arrive(&tempty[slot]);
       }
     }
+    if (lane == 0 && blockIdx.x == 0 && warp == 2 && dbg)
+      printf("epi warp: chunks %llu  ld+wait %.0f clk/chunk  wait_read %.0f clk/chunk  total-busy %.0f clk/chunk  tfull-wait %llu of %llu\n", n_chunk,
+             (double)t_ld / n_chunk, (double)t_wait / n_chunk, (double)(clock64() - t_all0 - t_tf) / n_chunk, t_tf, clock64() - t_all0);
   }
   if (warp >= 2 && lane == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
   tc_fence_before();
@@ -175,9 +185,9 @@ int main() {
   unsigned long long* out; cudaMalloc(&out, 148 * 8);
   const int ctas = 148;
   struct Cfg { int pair, N, S, KB, items, epi; } cfgs[] = {
-      {0, 256, 4, 12, 64, 0}, {0, 256, 4, 12, 64, 2}, {0, 256, 4, 12, 64, 1}, {0, 256, 4, 12, 64, 3}, {1, 256, 6, 12, 64, 3}, {0, 128, 6, 12, 64, 3}, {0, 128, 6, 12, 64, 0},
-      {1, 256, 6, 12, 64, 0}, {1, 256, 6, 12, 64, 2}, {1, 256, 6, 12, 64, 1},
-      {0, 256, 4, 64, 16, 1}, {1, 256, 6, 64, 16, 1}};
+      {0, 256, 4, 12, 64, 3}, {0, 256, 4, 12, 64, 2}, {0, 256, 4, 12, 64, 1}, {0, 128, 6, 12, 64, 3},
+      };
+  int dbg = 0;
   for (auto& c : cfgs) {
     Maps m;
     make(&m.a, buf, K, R, 128);
@@ -201,11 +211,13 @@ int main() {
     cudaError_t e;
     auto launch = [&](int items) {
       if (!c.pair) { cudaFuncSetAttribute(epi_kernel<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-        e = cudaLaunchKernelEx(&lc, epi_kernel<0>, m, items, c.KB, c.S, c.N, out, c.epi, C); }
+        e = cudaLaunchKernelEx(&lc, epi_kernel<0>, m, items, c.KB, c.S, c.N, out, c.epi, C, dbg); }
       else { cudaFuncSetAttribute(epi_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-        e = cudaLaunchKernelEx(&lc, epi_kernel<1>, m, items, c.KB, c.S, c.N, out, c.epi, C); }
+        e = cudaLaunchKernelEx(&lc, epi_kernel<1>, m, items, c.KB, c.S, c.N, out, c.epi, C, dbg); }
     };
+    dbg = 0;
     launch(4); cudaDeviceSynchronize();
+    dbg = 1;
     cudaEvent_t e0, e1; cudaEventCreate(&e0); cudaEventCreate(&e1);
     cudaEventRecord(e0); launch(c.items); cudaEventRecord(e1); cudaEventSynchronize(e1);
     float ms; cudaEventElapsedTime(&ms, e0, e1);
