@@ -210,20 +210,24 @@ ftb_status ftb_plan_batch(const ftb_hw* hw, const ftb_instance* insts, int32_t n
           // Parity mode ranks the final set only (an empty pool raises, as
           // combine.py:183-188 does). B200 mode walks a documented fallback
           // ladder when no combination covers tau: ranked set final -> filter
-          // -> cross -> align; then the same with the main-axis tile relaxed
-          // (any size <= 256, padded inside the MMA tile); then parity mode.
-          struct Rung { int legality, relax; };
+          // -> cross -> align; then the same with the main-axis tile relaxed,
+          // first to any wide MMA N (multiple of 32 in [128, 256]), then to any
+          // size <= 256 (padded inside the MMA tile); then parity mode.
+          // Reported stage = set index + 4 * rung.
+          struct Rung { int legality, relax, level; };
           std::vector<Rung> rungs;
           if (h.legality) {
-            rungs = {{1, -1}, {1, select_main_axis(in)}, {0, -1}};
+            const int tau = select_main_axis(in);
+            rungs = {{1, -1, 0}, {1, tau, 1}, {1, tau, 2}, {0, -1, 0}};
           } else {
-            rungs = {{0, -1}};
+            rungs = {{0, -1, 0}};
           }
           bool done = false;
           for (size_t ri = 0; ri < rungs.size() && !done; ++ri) {
             Hw hq = h;
             hq.legality = rungs[ri].legality;
             hq.relax_tau = rungs[ri].relax;
+            hq.relax_level = rungs[ri].level;
             const int last = h.legality ? 3 : 0;
             for (int stage = 0; stage <= last && !done; ++stage) {
               try {

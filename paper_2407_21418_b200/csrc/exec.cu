@@ -257,8 +257,9 @@ static void build(ExecImpl& ex, const ftb_gemm_desc* probs, const ftb_program* p
     P.num_kb = static_cast<int32_t>(ceil_div(d.K, kBlockK));
     if (ffma && !P.out_f32) throw input_error("FFMA mode writes fp32 outputs", "out_dtype");
 
-    // Orientation: fewest tensor-core MMA cells (lanes padded to 128, columns
-    // to 16 or 64), ties to the normal orientation.
+    // Orientation: least tensor-pipe time — per 128-lane slab and column piece
+    // an M=128 K=16 MMA costs max(kMmaFloorN, n_mma)/2 clk (B200 measurement,
+    // scripts/micro/mma_bench.cu); ties to the normal orientation.
     int swap = 0;
     if (!ffma) {
       int64_t cost[2] = {0, 0};
@@ -270,8 +271,8 @@ static void build(ExecImpl& ex, const ftb_gemm_desc* probs, const ftb_program* p
           const int64_t lane = o ? lj : li, col = o ? li : lj;
           split(0, col, kMaxN, cp);
           int64_t cols = 0;
-          for (auto& c : cp) cols += round_up(c.len, gran);
-          cost[o] += ceil_div(lane, kLaneRows) * kLaneRows * cols;
+          for (auto& c : cp) cols += std::max<int64_t>(kMmaFloorN, round_up(c.len, gran));
+          cost[o] += ceil_div(lane, kLaneRows) * cols;
         }
       }
       swap = d.orientation >= 0 ? d.orientation : (cost[1] < cost[0] ? 1 : 0);
@@ -330,9 +331,10 @@ static void build(ExecImpl& ex, const ftb_gemm_desc* probs, const ftb_program* p
             w.col_len = static_cast<int32_t>(Cc.len);
             w.n_mma = ffma ? static_cast<int32_t>(Cc.len) : static_cast<int32_t>(round_up(Cc.len, gran));
             w.aux = 0;
-            const int64_t cost = static_cast<int64_t>(P.num_kb) * (ffma ? L.len : kLaneRows) * w.n_mma;
+            const int64_t cells = static_cast<int64_t>(P.num_kb) * (ffma ? L.len : kLaneRows) * w.n_mma;
+            const int64_t cost = ffma ? cells : static_cast<int64_t>(P.num_kb) * std::max<int32_t>(kMmaFloorN, w.n_mma);
             items.push_back({cost, w});
-            ex.info.mma_flops += 2 * cost * kBlockK;
+            ex.info.mma_flops += 2 * cells * kBlockK;
           }
     }
     ex.info.true_flops += 2 * d.batch * d.M * d.N * d.K;

@@ -109,6 +109,7 @@ constexpr int kBlockK = 64;          // one 128-B swizzle atom of bf16 along K
 constexpr int kLaneRows = 128;       // MMA M
 constexpr int kMaxN = 256;           // MMA N upper bound
 constexpr int kMaxStages = 8;
+constexpr int kMmaFloorN = 200;      // an M=128 K=16 tcgen05.mma costs >= ~100 clk: N below this is not cheaper
 constexpr int kLaneStageBytes = kLaneRows * kBlockK * 2;   // 16 KiB
 constexpr int kTmemCols = 512;
 constexpr int kTcThreads = 192;                            // 6 warps

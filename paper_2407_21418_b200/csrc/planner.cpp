@@ -178,26 +178,37 @@ static std::vector<int64_t> reduce_options(int64_t e, int64_t align) {  // ukern
   return v;
 }
 
-bool tcgen05_legal(const Instance& in, const int64_t* smem, int relax_tau) {
+bool tcgen05_legal(const Instance& in, const int64_t* smem, int relax_tau, int relax_level) {
   // B200 extension: the uKernel's output tile must map onto efficient
   // tcgen05 tiles in one of the two orientations: 128 or 256 TMEM lanes
-  // (M = 128 per MMA) x 64..256 accumulator columns (MMA N, step 32); a tile
-  // spanning a whole short axis is also accepted. Batch tiles are free (one
-  // work item per batch entry); reduce tiles are whole 64-element TMA atoms.
+  // (M = 128 per MMA) x 256 accumulator columns (MMA N = 256); a tile spanning
+  // a whole short axis is also accepted. Measured on B200
+  // (scripts/micro/mma_bench.cu): a kind::f16 M=128 K=16 MMA costs ~100 clk
+  // whatever N <= 128 is (N=256: 128 clk), so narrower column tiles lose
+  // 25-70% of the tensor pipe; the C1 Dense step ran 1.59x faster with
+  // 256-column tiles (scripts/plan_variants.py). Batch tiles are free (one work
+  // item per batch entry); reduce tiles are whole 64-element TMA atoms.
   if (in.ns < 2) return false;
   const int ai = in.ns - 2, aj = in.ns - 1;
   const int64_t ti = smem[ai], tj = smem[aj], Ei = in.ext[ai], Ej = in.ext[aj];
   // lanes: full 128-lane MMA tiles (one or two), or one tile spanning a short axis
   auto lane_ok = [](int64_t t, int64_t E) { return (t % 128 == 0 && t <= 256) || (t >= E && t <= 128); };
-  // columns: N >= 64 in steps of 32 (the MMA-N sweet spot), or a whole short axis
-  auto col_ok = [](int64_t t, int64_t E) { return (t % 32 == 0 && t >= 64 && t <= 256) || (t >= E && t <= 256); };
+  // columns: the full MMA N = 256, or a whole short axis
+  auto col_ok = [](int64_t t, int64_t E) { return t == 256 || (t >= E && t <= 256); };
   for (int r = in.ns; r < in.na(); ++r)
     if (smem[r] % 64) return false;
   if (relax_tau == ai || relax_tau == aj) {
-    // fallback rung: the main-axis tile may take any size <= 256 (it is
-    // padded inside the MMA tile); the other output axis stays strict
     const int64_t t_tau = relax_tau == ai ? ti : tj, t_o = relax_tau == ai ? tj : ti;
-    const int64_t E_o = relax_tau == ai ? Ej : Ei;
+    const int64_t E_tau = relax_tau == ai ? Ei : Ej, E_o = relax_tau == ai ? Ej : Ei;
+    if (relax_level == 1) {
+      // first fallback rung: the main-axis tile may be any wide MMA N
+      // (multiple of 32 in [128, 256]) so that two parts can cover tau exactly;
+      // the other output axis stays strict in the matching role
+      auto col_wide = [](int64_t t, int64_t E) { return (t % 32 == 0 && t >= 128 && t <= 256) || (t >= E && t <= 256); };
+      return (col_wide(t_tau, E_tau) && lane_ok(t_o, E_o)) || (lane_ok(t_tau, E_tau) && col_ok(t_o, E_o));
+    }
+    // last fallback rung: the main-axis tile may take any size <= 256 (it is
+    // padded inside the MMA tile); the other output axis stays strict
     return t_tau <= 256 && (lane_ok(t_o, E_o) || col_ok(t_o, E_o));
   }
   return (lane_ok(ti, Ei) && col_ok(tj, Ej)) || (lane_ok(tj, Ej) && col_ok(ti, Ei));
@@ -294,7 +305,7 @@ Cands enumerate_legal(const Instance& in, const Hw& hw, int64_t cap, bool* trunc
   if (hw.legality) {  // B200 extension, applied right after enumeration + cap truncation
     std::vector<int64_t> keep;
     for (size_t i = 0; i < all.size(); ++i)
-      if (tcgen05_legal(in, all.smem_row(i), hw.relax_tau)) keep.push_back(static_cast<int64_t>(i));
+      if (tcgen05_legal(in, all.smem_row(i), hw.relax_tau, hw.relax_level)) keep.push_back(static_cast<int64_t>(i));
     subset_inplace(all, keep);
   }
   return all;

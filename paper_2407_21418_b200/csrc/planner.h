@@ -45,7 +45,8 @@ struct Instance {
 struct Hw {
   int64_t cores, regs, smem, bw_g, bw_s, peak, zeta, active, align;
   int legality;       // 0 parity, 1 tcgen05 legality (B200 mode)
-  int relax_tau = -1; // B200 fallback: space axis whose tile only needs t <= 256
+  int relax_tau = -1; // B200 fallback: space axis whose tile is relaxed
+  int relax_level = 2; // 1: tau tile may be any multiple of 32 in [128, 256] as MMA N; 2: any size <= 256
   static Hw from_c(const ftb_hw& h);
 };
 
@@ -103,7 +104,7 @@ std::vector<PlanRow> pool_export(const Cands& c, int tau);
 std::vector<std::pair<PlanRow, double>> rank_topk(const Cands& c, int tau, const ftb_coeffs& co,
                                                   int k, bool normalize);
 // B200 legality predicate (extension; parity mode never calls it).
-bool tcgen05_legal(const Instance& in, const int64_t* smem, int relax_tau = -1);
+bool tcgen05_legal(const Instance& in, const int64_t* smem, int relax_tau = -1, int relax_level = 2);
 
 }  // namespace plan
 }  // namespace ftb

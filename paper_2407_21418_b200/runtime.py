@@ -16,6 +16,7 @@ from __future__ import annotations
 
 import ctypes as C
 import json
+import os
 import threading
 import time
 from dataclasses import dataclass
@@ -30,7 +31,7 @@ from .mktune.hardware import HardwareDescriptor, b200_bf16, b200_ffma
 from .mktune.scoring import SiaCoeffs
 from .mktune.workload import WorkloadInstance, bmm_spec, dense_spec, workload_hash
 
-CACHE_VERSION = 1
+CACHE_VERSION = 2
 
 
 def dense_instance(M: int, N: int, K: int, elem_bytes: int = 2, m_max: int = 8192) -> WorkloadInstance:
@@ -73,13 +74,16 @@ class Planner:
                  coeffs: SiaCoeffs | None = None, threads: int = 0):
         self.hw = hw or b200_bf16(tcgen05=True)
         self.params = params or FilterParams.default()
+        if coeffs is None and os.environ.get("FTB_SIA_COEFFS"):
+            coeffs = SiaCoeffs(*(float(v) for v in os.environ["FTB_SIA_COEFFS"].split(",")))
         self.coeffs = coeffs or SiaCoeffs()
         self.threads = threads
         self._cache: dict[tuple, PlanRecord] = {}
         self._lock = threading.Lock()
 
     def _key(self, inst: WorkloadInstance) -> tuple:
-        return (self.hw.name, self.hw.tcgen05_mode, workload_hash(inst.spec), inst.binding_key())
+        c = self.coeffs
+        return (self.hw.name, self.hw.tcgen05_mode, (c.c0, c.c1, c.c2), workload_hash(inst.spec), inst.binding_key())
 
     def plan(self, instances: Sequence[WorkloadInstance]) -> list[PlanRecord]:
         """Top-1 program per instance (cached); misses are planned in one
@@ -166,7 +170,8 @@ class Planner:
             parts = [(p["reg"], p["smem"], p["count"]) for p in row["parts"]]
             g = program_struct(row["n_space"], row["tau"], parts, row["sia"])
             with self._lock:
-                self._cache[tuple(row["key"])] = PlanRecord(g, row["tuning_s"], row["relaxation"],
+                key = tuple(tuple(x) if isinstance(x, list) else x for x in row["key"])
+                self._cache[key] = PlanRecord(g, row["tuning_s"], row["relaxation"],
                                                             row["fallback_stage"], row["counts"])
             n += 1
         return n

@@ -30,7 +30,7 @@ def tcgen05_legal(space_axes, ext: dict, smem: dict) -> bool:
         return (t % 128 == 0 and t <= 256) or (t >= E and t <= 128)
 
     def col_ok(t, E):
-        return (t % 32 == 0 and 64 <= t <= 256) or (t >= E and t <= 256)
+        return t == 256 or (t >= E and t <= 256)
 
     if any(smem[a] % 64 for a in smem if a not in space_axes):
         return False
