@@ -6,6 +6,8 @@
 #include <cuda_bf16.h>
 #include <cstdint>
 
+#include "ptx.cuh"
+
 namespace ftb {
 
 __device__ __forceinline__ bool aligned16(const void* C, int64_t off, bool f32) {
@@ -158,4 +160,76 @@ __device__ __forceinline__ void stage_box_bf16(uint8_t* box, const uint32_t (&r)
           __float2bfloat16_rn(__uint_as_float(r[e]));
   }
 }
+
+// One epilogue warp's share of a finished work item: TMEM lanes
+// [lane_base, lane_base + 32) of the accumulator at `taddr`, columns
+// [0, col_len). C-side coordinates: normal orientation (swap = false) stores
+// lane l as C row lane0 + lane_base + l; swap-AB stores it as C column.
+// `release()` hands the accumulator back to the MMA warp right after the
+// last TMEM read. `region` is the warp's 8 KiB staging area (four 2 KiB TMA
+// boxes or the 32x33 fp32 transpose tile), `ngrp` its running box-group count.
+template <class Release>
+__device__ __forceinline__ void epilogue_tile(uint8_t* region, uint32_t& ngrp, uint32_t taddr, bool active, bool tma,
+                                              bool swap, bool f32, const CUtensorMap* out_map, void* C, int64_t ldc,
+                                              int lane0, int lane_len, int lane_base, int col0, int col_len, int batch,
+                                              Release release) {
+  const int lane = threadIdx.x & 31;
+  bool released = false;
+  if (active) {
+    if (tma) {
+      // groups of two 32-column chunks: both tcgen05.ld in flight, one proxy
+      // fence and one bulk group per pair of TMA stores
+      for (int c0 = 0; c0 < col_len; c0 += 64) {
+        const bool two = c0 + 32 < col_len;
+        uint32_t ra[32], rb[32];
+        tmem_ld_32x32b_x32(taddr + c0, ra);
+        if (two) tmem_ld_32x32b_x32(taddr + c0 + 32, rb);
+        tmem_ld_wait();
+        if (c0 + 64 >= col_len) {  // last TMEM read of the item
+          release();
+          released = true;
+        }
+        uint8_t* box = region + (ngrp & 1) * 4096;
+        if (lane == 0) bulk_wait_read<1>();  // the group that last used these boxes has read them
+        __syncwarp();
+        stage_box_bf16(box, ra, !swap);
+        if (two) stage_box_bf16(box + 2048, rb, !swap);
+        fence_async_smem();
+        __syncwarp();
+        if (lane == 0) {
+          const int l0 = lane0 + lane_base, k0 = col0 + c0;
+          if (!swap) {
+            tma_store_3d(out_map, smem_addr(box), k0, l0, batch);
+            if (two) tma_store_3d(out_map, smem_addr(box + 2048), k0 + 32, l0, batch);
+          } else {
+            tma_store_3d(out_map, smem_addr(box), l0, k0, batch);
+            if (two) tma_store_3d(out_map, smem_addr(box + 2048), l0, k0 + 32, batch);
+          }
+          bulk_commit();
+        }
+        ++ngrp;
+      }
+    } else {
+      float* tb = reinterpret_cast<float*>(region);
+      if (lane == 0) bulk_wait_read<0>();  // the transpose tile aliases this warp's store boxes
+      __syncwarp();
+      for (int c0 = 0; c0 < col_len; c0 += 32) {
+        uint32_t raw[32];
+        tmem_ld_32x32b_x32(taddr + c0, raw);
+        tmem_ld_wait();
+        float v[32];
+#pragma unroll
+        for (int e = 0; e < 32; ++e) v[e] = __uint_as_float(raw[e]);
+        const int ncol = min(32, col_len - c0);
+        const int nlane = min(32, lane_len - lane_base);
+        if (!swap)  // lanes = rows of C, TMEM columns = output columns
+          store_block32(tb, v, true, C, ldc, lane0 + lane_base, col0 + c0, nlane, ncol, f32);
+        else        // lanes = columns of C, TMEM columns = output rows
+          store_block32(tb, v, false, C, ldc, col0 + c0, lane0 + lane_base, ncol, nlane, f32);
+      }
+    }
+  }
+  if (!released) release();
+}
+
 }  // namespace ftb

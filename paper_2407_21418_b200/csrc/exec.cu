@@ -376,6 +376,16 @@ static void upload(ExecImpl& I) {
     const size_t esz = P.out_f32 ? 4 : 2;
     return static_cast<void*>(static_cast<char*>(P.C) + static_cast<int64_t>(batch) * P.c_bs * esz);
   };
+  // TMA stores write whole 32 x 32 boxes: legal for a rectangle whose extents
+  // are multiples of 32 or that ends at the tensor edge (the hardware clips).
+  const char* env_ts = std::getenv("FTB_TMA_STORE");
+  const bool tma_store_on = !(env_ts && env_ts[0] == '0');
+  auto tma_ok = [&](const DevWork& w) {
+    const DevProblem& P = I.problems[w.problem];
+    const int32_t lane_ext = P.swap ? P.N : P.M, col_ext = P.swap ? P.M : P.N;
+    return tma_store_on && I.tma_out[w.problem] && (w.lane_len % 32 == 0 || w.lane0 + w.lane_len == lane_ext) &&
+           (w.col_len % 32 == 0 || w.col0 + w.col_len == col_ext);
+  };
   // CTA pairs: logical items of one problem/batch with the same column range
   // share the column operand; group them (in cost order) two by two. Off by
   // default: measured on B200 the pair kernel loses to the single-CTA kernel
@@ -411,22 +421,12 @@ static void upload(ExecImpl& I) {
       t.n_mma = static_cast<int32_t>(round_up(w.col_len, P.col_mn ? 128 : 32));
       t.num_kb = P.num_kb;
       t.batch = w.batch;
-      t.flags = flags_of(P);
+      t.flags = flags_of(P) | (tma_ok(a) && tma_ok(w) ? kFlagTmaStore : 0u);
       pairs.push_back(t);
       paired[it->second] = paired[i] = 1;
       open.erase(it);
     }
   }
-  // TMA stores write whole 32 x 32 boxes: legal for a rectangle whose extents
-  // are multiples of 32 or that ends at the tensor edge (the hardware clips).
-  const char* env_ts = std::getenv("FTB_TMA_STORE");
-  const bool tma_store_on = !(env_ts && env_ts[0] == '0');
-  auto tma_ok = [&](const DevWork& w) {
-    const DevProblem& P = I.problems[w.problem];
-    const int32_t lane_ext = P.swap ? P.N : P.M, col_ext = P.swap ? P.M : P.N;
-    return tma_store_on && I.tma_out[w.problem] && (w.lane_len % 32 == 0 || w.lane0 + w.lane_len == lane_ext) &&
-           (w.col_len % 32 == 0 || w.col0 + w.col_len == col_ext);
-  };
   std::vector<TcWork> tw;
   int max_n = 16;
   for (size_t i = 0; i < I.work.size(); ++i) {
@@ -563,6 +563,7 @@ ftb_status ftb_exec_set_trace(ftb_exec* ex, int32_t enable) {
       FTB_CUDA(cudaMemset(I.d_trace, 0, n * sizeof(unsigned long long)));
     }
     I.cfg.trace = enable ? I.d_trace : nullptr;
+    I.cfg2.trace = enable ? I.d_trace : nullptr;
   });
 }
 

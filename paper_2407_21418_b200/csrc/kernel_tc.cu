@@ -54,6 +54,22 @@ __device__ __forceinline__ void trace_kb(const TcConfig& cfg, uint32_t g, int ev
         globaltimer();
 }
 
+// Work records are fetched one lane per 32-bit word (a coalesced 64-B load
+// whose latency overlaps the current item) and later broadcast from those
+// lanes with shfl: ptxas treats a shfl from a constant lane as warp-uniform,
+// so the loop bodies keep item fields in uniform registers. Warp converged.
+__device__ __forceinline__ uint32_t fetch_work_word(const TcWork* __restrict__ work, int w) {
+  const int lane = threadIdx.x & 31;
+  return lane < 16 ? __ldg(reinterpret_cast<const uint32_t*>(work + w) + lane) : 0u;
+}
+__device__ __forceinline__ TcWork bcast_work(uint32_t mine) {
+  TcWork it;
+  uint32_t* dst = reinterpret_cast<uint32_t*>(&it);
+#pragma unroll
+  for (int q = 0; q < 16; ++q) dst[q] = __shfl_sync(0xffffffffu, mine, q);
+  return it;
+}
+
 template <int S>
 __global__ void __launch_bounds__(kTcThreads, 1)
     ftb_tc_kernel(const TcWork* __restrict__ work, int32_t n_work, TcConfig cfg) {
@@ -93,39 +109,62 @@ __global__ void __launch_bounds__(kTcThreads, 1)
 
   if (warp == 0) {
     // ------------------------------------------------------------ producer
-    if (lane == 0) {
-      uint32_t g = 0;
-      uint32_t ps = 0, pphase = 0;  // producer ring slot / phase  // global K-block counter (ring position)
-      uint32_t local = 0;
-      TcWork nxt;
-      if (static_cast<int>(blockIdx.x) < n_work) nxt = load_work(work, blockIdx.x);
-      for (int w = blockIdx.x; w < n_work; w += G, ++local) {
-        const TcWork it = nxt;
-        if (w + G < n_work) {
-          nxt = load_work(work, w + G);
-        }
+    // The whole warp walks the loops with warp-uniform values (work records
+    // broadcast from lane 0 with shfl, so ptxas keeps them in uniform
+    // registers); lane 0 alone arms the barrier and issues the TMA loads.
+    // Records are fetched two items ahead so the next item's descriptor
+    // prefetch never waits on a global load.
+    uint32_t g = 0;
+    uint32_t ps = 0, pphase = 0;  // ring slot / phase
+    uint32_t local = 0;
+#ifdef FTB_PROD_PROFILE
+    unsigned long long c_wait = 0, c_issue = 0, c_item = 0, c_t0 = clock64();
+#endif
+    TcWork cur, nxt;
+    uint32_t pend = 0;  // raw word of the record two items ahead
+    if (static_cast<int>(blockIdx.x) < n_work) cur = bcast_work(fetch_work_word(work, blockIdx.x));
+    if (static_cast<int>(blockIdx.x) + G < n_work) nxt = bcast_work(fetch_work_word(work, blockIdx.x + G));
+    if (static_cast<int>(blockIdx.x) + 2 * G < n_work) pend = fetch_work_word(work, blockIdx.x + 2 * G);
+    for (int w = blockIdx.x; w < n_work; w += G, ++local) {
+      const TcWork it = cur;
+      if (lane == 0) {
         trace_ev(cfg, local, 0);
-        const CUtensorMap* tl = &it.maps->lane;
         if (w + G < n_work) {
           tma_prefetch_desc(&nxt.maps->lane);
           tma_prefetch_desc(&nxt.maps->col[0]);
         }
-        const bool lane_mn = it.flags & kFlagLaneMN, col_mn = it.flags & kFlagColMN;
-        const uint32_t bytes = kLaneStageBytes + static_cast<uint32_t>(it.n_mma) * kBlockK * 2;
-        const uint32_t cmask = col_box_mask(it.n_mma);
-        int boff[kColMaps];  // smem row offset of each column box (widest first)
-        {
-          int r = 0;
+      }
+      const CUtensorMap* tl = &it.maps->lane;
+      const bool lane_mn = it.flags & kFlagLaneMN, col_mn = it.flags & kFlagColMN;
+      const uint32_t bytes = kLaneStageBytes + static_cast<uint32_t>(it.n_mma) * kBlockK * 2;
+      const uint32_t cmask = col_box_mask(it.n_mma);
+      int boff[kColMaps];  // smem row offset of each column box (widest first)
+      {
+        int r = 0;
 #pragma unroll
-          for (int q = 0; q < kColMaps; ++q) {
-            boff[q] = r;
-            if (cmask & (1u << q)) r += 256 >> q;
-          }
+        for (int q = 0; q < kColMaps; ++q) {
+          boff[q] = r;
+          if (cmask & (1u << q)) r += 256 >> q;
         }
-        for (int kb = 0; kb < it.num_kb; ++kb, ++g) {
-          const uint32_t s = ps;
-          mbar_wait(&empty[s], pphase ^ 1);
-          if (++ps == S) { ps = 0; pphase ^= 1; }
+      }
+#ifdef FTB_PROD_PROFILE
+      unsigned long long ci = clock64();
+#endif
+      for (int kb = 0; kb < it.num_kb; ++kb, ++g) {
+        const uint32_t s = ps;
+#ifdef FTB_PROD_PROFILE
+        unsigned long long cw = clock64();
+#endif
+        mbar_wait(&empty[s], pphase ^ 1);
+        if (++ps == S) { ps = 0; pphase ^= 1; }
+#ifdef FTB_PROD_PROFILE
+        unsigned long long cs = clock64();
+        c_wait += cs - cw;
+#endif
+        if (lane == 0) {
+#ifdef FTB_TRACE_ISSUE
+          trace_kb(cfg, g, 1);  // debug: time before the TMA issue (replaces "MMA saw data")
+#endif
           mbar_arrive_expect_tx(&full[s], bytes);
           uint8_t* ldst = lane_buf + s * kLaneStageBytes;
           uint8_t* cdst = col_buf + s * cfg.col_stage_bytes;
@@ -148,34 +187,53 @@ __global__ void __launch_bounds__(kTcThreads, 1)
           if (kb == 0) trace_ev(cfg, local, 1);
           trace_kb(cfg, g, 0);
         }
+        __syncwarp();
+#ifdef FTB_PROD_PROFILE
+        c_issue += clock64() - cs;
+#endif
       }
+#ifdef FTB_PROD_PROFILE
+      c_item += clock64() - ci;
+#endif
+      cur = nxt;
+      if (w + 2 * G < n_work) nxt = bcast_work(pend);
+      if (w + 3 * G < n_work) pend = fetch_work_word(work, w + 3 * G);
     }
+#ifdef FTB_PROD_PROFILE
+    if (lane == 0 && cfg.trace) {
+      unsigned long long* t = cfg.trace + static_cast<size_t>(blockIdx.x) * kTracePerCta;
+      t[0] = c_wait; t[1] = c_issue; t[2] = c_item; t[3] = g; t[4] = local; t[5] = clock64() - c_t0;
+    }
+#endif
   } else if (warp == 1) {
     // ------------------------------------------------------------ MMA issuer
-    if (lane == 0) {
-      uint32_t g = 0;
-      uint32_t ms = 0, mphase = 0;  // MMA ring slot / phase
-      uint32_t local = 0;
-      TcWork nxt;
-      if (static_cast<int>(blockIdx.x) < n_work) nxt = load_work(work, blockIdx.x);
-      for (int w = blockIdx.x; w < n_work; w += G, ++local) {
-        const TcWork it = nxt;
-        if (w + G < n_work) nxt = load_work(work, w + G);
-        const uint32_t slot = local % cfg.n_acc;
-        const uint32_t use = local / cfg.n_acc;
-        const uint32_t lane_mn = (it.flags & kFlagLaneMN) ? 1u : 0u;
-        const uint32_t col_mn = (it.flags & kFlagColMN) ? 1u : 0u;
-        mbar_wait(&tempty[slot], (use & 1) ^ 1);
+    // whole warp walks the loops (uniform values); lane 0 issues and commits
+    uint32_t g = 0;
+    uint32_t ms = 0, mphase = 0;  // MMA ring slot / phase
+    uint32_t local = 0;
+    uint32_t pend = 0;
+    if (static_cast<int>(blockIdx.x) < n_work) pend = fetch_work_word(work, blockIdx.x);
+    for (int w = blockIdx.x; w < n_work; w += G, ++local) {
+      const TcWork it = bcast_work(pend);
+      if (w + G < n_work) pend = fetch_work_word(work, w + G);  // lands while this item runs
+      const uint32_t slot = local % cfg.n_acc;
+      const uint32_t use = local / cfg.n_acc;
+      const uint32_t lane_mn = (it.flags & kFlagLaneMN) ? 1u : 0u;
+      const uint32_t col_mn = (it.flags & kFlagColMN) ? 1u : 0u;
+      mbar_wait(&tempty[slot], (use & 1) ^ 1);
+      tc_fence_after();
+      const uint32_t tmem_d = tmem_base + slot * cfg.acc_cols;
+      const uint32_t idesc = idesc_bf16_f32(kLaneRows, static_cast<uint32_t>(it.n_mma), lane_mn, col_mn);
+      for (int kb = 0; kb < it.num_kb; ++kb, ++g) {
+        const uint32_t s = ms;
+        mbar_wait(&full[s], mphase);
+        if (++ms == S) { ms = 0; mphase ^= 1; }
         tc_fence_after();
-        const uint32_t tmem_d = tmem_base + slot * cfg.acc_cols;
-        const uint32_t idesc = idesc_bf16_f32(kLaneRows, static_cast<uint32_t>(it.n_mma), lane_mn, col_mn);
-        for (int kb = 0; kb < it.num_kb; ++kb, ++g) {
-          const uint32_t s = ms;
-          mbar_wait(&full[s], mphase);
-          if (++ms == S) { ms = 0; mphase ^= 1; }
-          tc_fence_after();
+        if (lane == 0) {
           if (kb == 0) trace_ev(cfg, local, 2);
+#ifndef FTB_TRACE_ISSUE
           trace_kb(cfg, g, 1);
+#endif
           const uint32_t la = smem_addr(lane_buf + s * kLaneStageBytes);
           const uint32_t ca = smem_addr(col_buf + s * cfg.col_stage_bytes);
 #pragma unroll
@@ -188,9 +246,13 @@ __global__ void __launch_bounds__(kTcThreads, 1)
           }
           tc_commit(&empty[s]);  // frees the smem slot when these MMAs finish
         }
+        __syncwarp();
+      }
+      if (lane == 0) {
         tc_commit(&tfull[slot]);  // accumulator ready for the epilogue
         trace_ev(cfg, local, 3);
       }
+      __syncwarp();
     }
   } else {
     // ------------------------------------------------------------ epilogue
@@ -198,7 +260,6 @@ __global__ void __launch_bounds__(kTcThreads, 1)
     // per-warp 8 KiB staging region: four 2 KiB TMA store boxes (two groups of
     // two), or — for predicated items — the 32x33 fp32 transpose tile (aliased)
     uint8_t* region = reinterpret_cast<uint8_t*>(epi_buf) + quad * kEpiWarpBytes;
-    float* tb = reinterpret_cast<float*>(region);
     uint32_t local = 0, ngrp = 0;
     TcWork nxt;
     if (static_cast<int>(blockIdx.x) < n_work) nxt = load_work(work, blockIdx.x);
@@ -213,68 +274,13 @@ __global__ void __launch_bounds__(kTcThreads, 1)
       tc_fence_after();
       if (quad == 0 && lane == 0) trace_ev(cfg, local, 4);
       const int lane_base = quad * 32;
-      bool released = false;
-      if (lane_base < it.lane_len) {
-        const uint32_t taddr = tmem_base + (static_cast<uint32_t>(lane_base) << 16) + slot * cfg.acc_cols;
-        if (tma) {
-          // groups of two 32-column chunks: both tcgen05.ld in flight, one
-          // proxy fence and one bulk group per pair of TMA stores
-          for (int c0 = 0; c0 < it.col_len; c0 += 64) {
-            const bool two = c0 + 32 < it.col_len;
-            uint32_t ra[32], rb[32];
-            tmem_ld_32x32b_x32(taddr + c0, ra);
-            if (two) tmem_ld_32x32b_x32(taddr + c0 + 32, rb);
-            tmem_ld_wait();
-            if (c0 + 64 >= it.col_len) {  // last TMEM read of the item: hand the slot back now
-              tc_fence_before();
-              __syncwarp();
-              if (lane == 0) mbar_arrive(&tempty[slot]);
-              released = true;
-            }
-            uint8_t* box = region + (ngrp & 1) * 4096;
-            if (lane == 0) bulk_wait_read<1>();  // the group that last used these boxes has read them
-            __syncwarp();
-            stage_box_bf16(box, ra, !swap);
-            if (two) stage_box_bf16(box + 2048, rb, !swap);
-            fence_async_smem();
-            __syncwarp();
-            if (lane == 0) {
-              const int l0 = it.lane0 + lane_base, k0 = it.col0 + c0;
-              if (!swap) {
-                tma_store_3d(&it.maps->out, smem_addr(box), k0, l0, it.batch);
-                if (two) tma_store_3d(&it.maps->out, smem_addr(box + 2048), k0 + 32, l0, it.batch);
-              } else {
-                tma_store_3d(&it.maps->out, smem_addr(box), l0, k0, it.batch);
-                if (two) tma_store_3d(&it.maps->out, smem_addr(box + 2048), l0, k0 + 32, it.batch);
-              }
-              bulk_commit();
-            }
-            ++ngrp;
-          }
-        } else {
-          if (lane == 0) bulk_wait_read<0>();  // the transpose tile aliases this warp's store boxes
-          __syncwarp();
-          for (int c0 = 0; c0 < it.col_len; c0 += 32) {
-            uint32_t raw[32];
-            tmem_ld_32x32b_x32(taddr + c0, raw);
-            tmem_ld_wait();
-            float v[32];
-#pragma unroll
-            for (int e = 0; e < 32; ++e) v[e] = __uint_as_float(raw[e]);
-            const int ncol = min(32, it.col_len - c0);
-            const int nlane = min(32, it.lane_len - lane_base);
-            if (!swap)  // lanes = rows of C, TMEM columns = output columns
-              store_block32(tb, v, true, it.C, it.ldc, it.lane0 + lane_base, it.col0 + c0, nlane, ncol, f32);
-            else        // lanes = columns of C, TMEM columns = output rows
-              store_block32(tb, v, false, it.C, it.ldc, it.col0 + c0, it.lane0 + lane_base, ncol, nlane, f32);
-          }
-        }
-      }
-      if (!released) {
-        tc_fence_before();
-        __syncwarp();
-        if (lane == 0) mbar_arrive(&tempty[slot]);
-      }
+      const uint32_t taddr = tmem_base + (static_cast<uint32_t>(lane_base) << 16) + slot * cfg.acc_cols;
+      epilogue_tile(region, ngrp, taddr, lane_base < it.lane_len, tma, swap, f32, &it.maps->out, it.C, it.ldc,
+                    it.lane0, it.lane_len, lane_base, it.col0, it.col_len, it.batch, [&] {
+                      tc_fence_before();
+                      __syncwarp();
+                      if (lane == 0) mbar_arrive(&tempty[slot]);
+                    });
       if (quad == 0 && lane == 0) trace_ev(cfg, local, 5);
     }
     if (lane == 0) bulk_wait_all();  // output stores complete before the CTA retires

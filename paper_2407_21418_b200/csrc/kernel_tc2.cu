@@ -36,6 +36,16 @@ __device__ __forceinline__ TcPair load_pair(const TcPair* __restrict__ work, int
   return it;
 }
 
+__device__ __forceinline__ void trace2_ev(const TcConfig& cfg, uint32_t local, int ev) {
+  if (cfg.trace && local < kTraceItems)
+    cfg.trace[static_cast<size_t>(blockIdx.x) * kTracePerCta + local * kTraceEvents + ev] = globaltimer();
+}
+__device__ __forceinline__ void trace2_kb(const TcConfig& cfg, uint32_t g, int ev) {
+  if (cfg.trace && g < kTraceKb)
+    cfg.trace[static_cast<size_t>(blockIdx.x) * kTracePerCta + kTraceItems * kTraceEvents + 2 * g + ev] =
+        globaltimer();
+}
+
 template <int S>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kTcThreads, 1)
     ftb_tc2_kernel(const TcPair* __restrict__ work, int32_t n_work, TcConfig cfg) {
@@ -81,11 +91,19 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kTcThreads, 1)
     if (lane == 0) {
       uint32_t g = 0;
       uint32_t ps = 0, pphase = 0;  // producer ring slot / phase
+      uint32_t local = 0;
+#ifdef FTB_PROD_PROFILE
+      unsigned long long c_wait = 0, c_issue = 0, c_item = 0, c_t0 = clock64();
+#endif
       TcPair nxt;
       if (cid < n_work) nxt = load_pair(work, cid);
-      for (int w = cid; w < n_work; w += G) {
+      for (int w = cid; w < n_work; w += G, ++local) {
         const TcPair it = nxt;
         if (w + G < n_work) nxt = load_pair(work, w + G);
+        trace2_ev(cfg, local, 0);
+#ifdef FTB_PROD_PROFILE
+        unsigned long long ci = clock64();
+#endif
         const bool lane_mn = it.flags & kFlagLaneMN, col_mn = it.flags & kFlagColMN;
         const int half = it.n_mma >> 1;
         const int lane0 = rank ? it.lane0[1] : it.lane0[0];
@@ -103,9 +121,16 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kTcThreads, 1)
         }
         for (int kb = 0; kb < it.num_kb; ++kb, ++g) {
           const uint32_t s = ps;
+#ifdef FTB_PROD_PROFILE
+          unsigned long long cw = clock64();
+#endif
           mbar_wait(&empty[s], pphase ^ 1);
           if (++ps == S) { ps = 0; pphase ^= 1; }
-          const uint32_t fb = mapa_shared(smem_addr(&full[s]), 0);
+#ifdef FTB_PROD_PROFILE
+          unsigned long long cs = clock64();
+          c_wait += cs - cw;
+#endif
+          const uint32_t fb = smem_addr(&full[s]) & kPeerBitMask;  // leader's barrier
           if (leader) mbar_arrive_expect_tx(&full[s], 2 * bytes_cta);
           uint8_t* ldst = lane_buf + s * kLaneStageBytes;
           uint8_t* cdst = col_buf + s * cfg.col_stage_bytes;
@@ -125,8 +150,22 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kTcThreads, 1)
             for (int c = 0; c < half; c += 64)
               tma_load_3d_pair(cdst + c * 128, &it.maps->col[0], fb, colr + c, k0, it.batch);
           }
+          if (kb == 0) trace2_ev(cfg, local, 1);
+          trace2_kb(cfg, g, 0);
+#ifdef FTB_PROD_PROFILE
+          c_issue += clock64() - cs;
+#endif
         }
+#ifdef FTB_PROD_PROFILE
+        c_item += clock64() - ci;
+#endif
       }
+#ifdef FTB_PROD_PROFILE
+      if (cfg.trace) {
+        unsigned long long* t = cfg.trace + static_cast<size_t>(blockIdx.x) * kTracePerCta;
+        t[0] = c_wait; t[1] = c_issue; t[2] = c_item; t[3] = g; t[4] = local; t[5] = clock64() - c_t0;
+      }
+#endif
     }
   } else if (warp == 1) {
     // ------------------------------------------------------------ MMA issuer (leader)
@@ -152,6 +191,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kTcThreads, 1)
           mbar_wait(&full[s], mphase);
           if (++ms == S) { ms = 0; mphase ^= 1; }
           tc_fence_after();
+          if (kb == 0) trace2_ev(cfg, local, 2);
+          trace2_kb(cfg, g, 1);
           const uint32_t la = smem_addr(lane_buf + s * kLaneStageBytes);
           const uint32_t ca = smem_addr(col_buf + s * cfg.col_stage_bytes);
 #pragma unroll
@@ -165,13 +206,14 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kTcThreads, 1)
           tc_commit_pair_mc(&empty[s]);
         }
         tc_commit_pair_mc(&tfull[slot]);
+        trace2_ev(cfg, local, 3);
       }
     }
   } else {
     // ------------------------------------------------------------ epilogue (both CTAs)
     const int quad = warp & 3;
-    float* tb = epi_buf + quad * (kEpiWarpBytes / 4);
-    uint32_t local = 0;
+    uint8_t* region = reinterpret_cast<uint8_t*>(epi_buf) + quad * kEpiWarpBytes;
+    uint32_t local = 0, ngrp = 0;
     TcPair nxt;
     if (cid < n_work) nxt = load_pair(work, cid);
     for (int w = cid; w < n_work; w += G, ++local) {
@@ -180,32 +222,24 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kTcThreads, 1)
       const uint32_t slot = local % cfg.n_acc;
       const uint32_t use = local / cfg.n_acc;
       const bool swap = it.flags & kFlagSwap, f32 = it.flags & kFlagOutF32;
+      const bool tma = it.flags & kFlagTmaStore;
       const int lane_len = rank ? it.lane_len[1] : it.lane_len[0];
       const int lane0 = rank ? it.lane0[1] : it.lane0[0];
       mbar_wait(&tfull[slot], use & 1);
       tc_fence_after();
+      if (quad == 0 && lane == 0) trace2_ev(cfg, local, 4);
       const int lane_base = quad * 32;
-      if (lane_base < lane_len) {
-        const uint32_t taddr = tmem_base + (static_cast<uint32_t>(lane_base) << 16) + slot * cfg.acc_cols;
-        for (int c0 = 0; c0 < it.col_len; c0 += 32) {
-          uint32_t raw[32];
-          tmem_ld_32x32b_x32(taddr + c0, raw);
-          tmem_ld_wait();
-          float v[32];
-#pragma unroll
-          for (int e = 0; e < 32; ++e) v[e] = __uint_as_float(raw[e]);
-          const int ncol = min(32, it.col_len - c0);
-          const int nlane = min(32, lane_len - lane_base);
-          if (!swap)  // lanes = rows of C, TMEM columns = output columns
-            store_block32(tb, v, true, it.C, it.ldc, lane0 + lane_base, it.col0 + c0, nlane, ncol, f32);
-          else        // lanes = columns of C, TMEM columns = output rows
-            store_block32(tb, v, false, it.C, it.ldc, it.col0 + c0, lane0 + lane_base, ncol, nlane, f32);
-        }
-      }
-      tc_fence_before();
-      __syncwarp();
-      if (lane == 0) mbar_arrive_cluster(mapa_shared(smem_addr(&tempty[slot]), 0));
+      const uint32_t taddr = tmem_base + (static_cast<uint32_t>(lane_base) << 16) + slot * cfg.acc_cols;
+      epilogue_tile(region, ngrp, taddr, lane_base < lane_len, tma, swap, f32, &it.maps->out, it.C, it.ldc, lane0,
+                    lane_len, lane_base, it.col0, it.col_len, it.batch, [&] {
+                      tc_fence_before();
+                      __syncwarp();
+                      if (lane == 0) mbar_arrive_remote(smem_addr(&tempty[slot]) & kPeerBitMask);
+                    });
+      if (quad == 0 && lane == 0) trace2_ev(cfg, local, 5);
     }
+    if (lane == 0) bulk_wait_all();  // output stores complete before the CTA retires
+    __syncwarp();
   }
 
   tc_fence_before();

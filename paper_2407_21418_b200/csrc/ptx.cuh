@@ -167,6 +167,15 @@ __device__ __forceinline__ void cluster_sync() {
 __device__ __forceinline__ void mbar_arrive_cluster(uint32_t cluster_addr) {
   asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr) : "memory");
 }
+// remote arrive with the default .release.cta semantics (as CUTLASS's
+// ClusterBarrier::arrive(cta_id)); .release.cluster costs a cluster-scope
+// fence (~700 clk measured in scripts/micro/tma_bench.cu)
+__device__ __forceinline__ void mbar_arrive_remote(uint32_t cluster_addr) {
+  asm volatile("mbarrier.arrive.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr) : "memory");
+}
+// In a CTA pair the shared::cta window address with bit 24 cleared names the
+// same variable in the even (leader) CTA (cf. CUTLASS Sm100MmaPeerBitMask).
+constexpr uint32_t kPeerBitMask = 0xFEFFFFFFu;
 // 2-SM TMA load: data lands in this CTA's smem, completion bytes are counted
 // on the mbarrier at `bar_cluster` (the leader CTA's barrier).
 __device__ __forceinline__ void tma_load_3d_pair(void* dst, const CUtensorMap* m, uint32_t bar_cluster,

@@ -15,8 +15,8 @@ struct Maps { CUtensorMap a; CUtensorMap b; };
 
 template <int MODE, int MASK = 0>  // 0 single-CTA, 1 cluster-2 with cta_group::2 TMA, 2 cluster-2 plain TMA
 __global__ void __launch_bounds__(192, 1) tma_kernel(const __grid_constant__ Maps maps_p, int iters, int S,
-                                                    int a_rows, int b_rows, unsigned long long* out, const Maps* gmaps) {
-  const Maps& maps = gmaps ? *gmaps : maps_p;
+                                                    int a_rows, int b_rows, unsigned long long* out, const Maps* gmaps, int ndesc) {
+  const Maps& maps0 = gmaps ? *gmaps : maps_p;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   const int stage_bytes = (a_rows + b_rows) * 128;
@@ -38,6 +38,7 @@ __global__ void __launch_bounds__(192, 1) tma_kernel(const __grid_constant__ Map
       mbar_wait(&empty[ps], ph ^ 1);
       uint8_t* dst = smem + ps * stage_bytes;
       int k0 = (it % 64) * 64;
+      const Maps& maps = (gmaps && ndesc > 1) ? gmaps[(it + blockIdx.x) % ndesc] : maps0;
       int row = ((blockIdx.x * 7 + it / 64) % 16) * 256;
       if (MODE == 1) {
         uint32_t fb = MASK ? (smem_addr(&full[ps]) & 0xFEFFFFFFu) : mapa_shared(smem_addr(&full[ps]), 0);
@@ -91,9 +92,9 @@ int main() {
   void* buf; cudaMalloc(&buf, K * R * 2); cudaMemset(buf, 0, K * R * 2);
   unsigned long long* out; cudaMalloc(&out, 148 * 8);
   int ctas = 148, iters = 2000;
-  Maps* dmaps; cudaMalloc(&dmaps, sizeof(Maps));
+  Maps* dmaps; cudaMalloc(&dmaps, 512 * sizeof(Maps));
   struct Cfg { int mode, a, b, S; const char* name; int gm = 0; int spin = 0; } cfgs[] = {
-      {0, 128, 128, 6, "GMEM-desc single 128+128 S6", 1}, {0, 128, 128, 6, "single + 4 spinning warps", 0, 1}, {0, 128, 256, 4, "single 128+256 + 4 spinning warps", 0, 1}, {1, 128, 128, 6, "GMEM-desc pair 128+128 S6", 1},
+      {0, 128, 128, 6, "GMEM-desc single 128+128 S6", 1}, {0, 128, 128, 6, "GMEM 8 descs", 8}, {0, 128, 128, 6, "GMEM 64 descs", 64}, {0, 128, 128, 6, "GMEM 512 descs", 512}, {0, 128, 128, 6, "single + 4 spinning warps", 0, 1}, {0, 128, 256, 4, "single 128+256 + 4 spinning warps", 0, 1}, {1, 128, 128, 6, "GMEM-desc pair 128+128 S6", 1},
       {0, 128, 256, 4, "single 128+256 S4"}, {0, 128, 128, 6, "single 128+128 S6"}, {0, 128, 64, 8, "single 128+64 S8"},
       {0, 128, 0, 8, "single 128 only S8"}, {0, 256, 0, 6, "single 256 only S6"},
       {1, 128, 128, 6, "pair(cta_group::2) 128+128 S6"}, {1, 128, 64, 8, "pair 128+64 S8"}, {3, 128, 128, 6, "pair masked-bar 128+128 S6"},
@@ -103,7 +104,7 @@ int main() {
     Maps m;
     make(&m.a, buf, K, R, c.a > 0 ? (c.a > 256 ? 256 : c.a) : 64);
     make(&m.b, buf, K, R, c.b > 0 ? c.b : 64);
-    cudaMemcpy(dmaps, &m, sizeof(Maps), cudaMemcpyHostToDevice);
+    for (int d = 0; d < 512; ++d) cudaMemcpy(dmaps + d, &m, sizeof(Maps), cudaMemcpyHostToDevice);
     int smem = c.S * (c.a + c.b) * 128 + 2048;
     cudaLaunchConfig_t lc = {};
     lc.gridDim = dim3(ctas); lc.blockDim = dim3(c.spin ? 192 : 64); lc.dynamicSmemBytes = smem;
@@ -114,13 +115,13 @@ int main() {
     cudaError_t e;
     auto launch = [&](int it) {
       if (c.mode == 0) { cudaFuncSetAttribute(tma_kernel<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-        e = cudaLaunchKernelEx(&lc, tma_kernel<0>, m, it, c.S, c.a, c.b, out, c.gm ? dmaps : nullptr); }
+        e = cudaLaunchKernelEx(&lc, tma_kernel<0>, m, it, c.S, c.a, c.b, out, c.gm ? dmaps : nullptr, c.gm); }
       else if (c.mode == 3) { cudaFuncSetAttribute(tma_kernel<1, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-        e = cudaLaunchKernelEx(&lc, tma_kernel<1, 1>, m, it, c.S, c.a, c.b, out, c.gm ? dmaps : nullptr); }
+        e = cudaLaunchKernelEx(&lc, tma_kernel<1, 1>, m, it, c.S, c.a, c.b, out, c.gm ? dmaps : nullptr, c.gm); }
       else if (c.mode == 1) { cudaFuncSetAttribute(tma_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-        e = cudaLaunchKernelEx(&lc, tma_kernel<1>, m, it, c.S, c.a, c.b, out, c.gm ? dmaps : nullptr); }
+        e = cudaLaunchKernelEx(&lc, tma_kernel<1>, m, it, c.S, c.a, c.b, out, c.gm ? dmaps : nullptr, c.gm); }
       else { cudaFuncSetAttribute(tma_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-        e = cudaLaunchKernelEx(&lc, tma_kernel<2>, m, it, c.S, c.a, c.b, out, c.gm ? dmaps : nullptr); }
+        e = cudaLaunchKernelEx(&lc, tma_kernel<2>, m, it, c.S, c.a, c.b, out, c.gm ? dmaps : nullptr, c.gm); }
     };
     launch(100); cudaDeviceSynchronize();
     cudaEvent_t e0, e1; cudaEventCreate(&e0); cudaEventCreate(&e1);
