@@ -58,7 +58,7 @@ PFN_cuTensorMapEncodeTiled_v12000 get_encode() {
 // 3-D bf16 tensor map: dims {inner, rows, batch}, SWIZZLE_128B, OOB = zeros.
 void encode_map(CUtensorMap* m, const void* base, int64_t inner, int64_t rows, int64_t batch,
                 int64_t ld_elems, int64_t batch_stride_elems, uint32_t box_inner,
-                uint32_t box_rows) {
+                uint32_t box_rows, uint32_t box_batch = 1) {
   if (reinterpret_cast<uintptr_t>(base) % 16)
     throw input_error("tcgen05 path needs 16-byte aligned operand base pointers", "A/B");
   if ((ld_elems * 2) % 16)
@@ -69,7 +69,7 @@ void encode_map(CUtensorMap* m, const void* base, int64_t inner, int64_t rows, i
   int64_t bs = batch > 1 ? batch_stride_elems : rows * ld_elems;
   if ((bs * 2) % 16) throw input_error("batch stride must be a multiple of 8 elements", "batch");
   cuuint64_t strides[2] = {static_cast<cuuint64_t>(ld_elems * 2), static_cast<cuuint64_t>(bs * 2)};
-  cuuint32_t box[3] = {box_inner, box_rows, 1};
+  cuuint32_t box[3] = {box_inner, box_rows, box_batch};
   cuuint32_t estr[3] = {1, 1, 1};
   CUresult r = get_encode()(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<void*>(base), dims,
                             strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
@@ -198,6 +198,8 @@ struct ExecImpl {
   DevWork* d_work = nullptr;
   DevMaps* d_maps = nullptr;
   std::vector<uint8_t> tma_out;       // per problem: C store map usable
+  std::vector<int32_t> pack_depth;    // per problem: batch entries per TMA box (1 = no packing)
+  std::vector<int32_t> pack_rows;     // per problem: lane box rows when packed
   TcWork* d_tcwork = nullptr;
   TcPair* d_tcpairs = nullptr;
   unsigned long long* d_trace = nullptr;
@@ -281,6 +283,33 @@ static void build(ExecImpl& ex, const ftb_gemm_desc* probs, const ftb_program* p
     P.lane_mn = swap && !P.b_nk;
     P.col_mn = !swap && !P.b_nk;
     if (!ffma && d.in_dtype != FTB_DT_BF16) throw input_error("unsupported input dtype", "in_dtype");
+    // Batch packing: a BMM whose every batch entry is one work piece (lane
+    // extent <= 128, column extent <= 256, K-major lane operand, and a column
+    // operand that is K-major or a single 64-wide MN-major box) runs up to
+    // kMaxPack consecutive entries per work item, loaded by one 3-D TMA box per
+    // operand and K block (the box's third dimension is the batch).
+    int32_t depth = 1, lrows = 0;
+    if (!ffma && d.op == FTB_OP_BMM && !P.lane_mn) {
+      const int64_t lane_ext = swap ? d.N : d.M, col_ext = swap ? d.M : d.N;
+      bool one_piece = true;
+      for (const Region& r : regs) {
+        const int64_t li = r.hi[ib] - r.lo[ib], lj = r.hi[ib + 1] - r.lo[ib + 1];
+        if ((swap ? lj : li) != lane_ext || (swap ? li : lj) != col_ext) one_piece = false;
+      }
+      const int64_t ncols = P.col_mn ? 64 : round_up(col_ext, 16);
+      if (one_piece && lane_ext <= kLaneRows && (!P.col_mn || col_ext <= 64) && ncols <= kMaxN) {
+        lrows = static_cast<int32_t>(round_up(lane_ext, 16));
+        const int64_t cstride = round_up(ncols, 32);
+        const char* pm = std::getenv("FTB_PACK_MAX");
+        const int64_t pack_max = pm ? std::max(1, std::min(kMaxPack, std::atoi(pm))) : kMaxPack;
+        int64_t nb = std::min<int64_t>({pack_max, kLaneRows / lrows, kMaxN / ncols, kMaxN / cstride,
+                                        static_cast<int64_t>(d.batch)});
+        const int64_t c_bs = d.c_batch_stride;
+        if (nb >= 2 && c_bs < (int64_t(1) << 31) && !std::getenv("FTB_NO_PACK")) depth = static_cast<int32_t>(nb);
+      }
+    }
+    ex.pack_depth.push_back(depth);
+    ex.pack_rows.push_back(lrows);
     if (!ffma && encode) {
       // A: [batch][M][lda], K contiguous. B: [batch][N][ldb] (NK) or [batch][K][ldb] (KN).
       DevMaps m;
@@ -291,15 +320,25 @@ static void build(ExecImpl& ex, const ftb_gemm_desc* probs, const ftb_program* p
       const int64_t lane_ld = swap ? d.ldb : d.lda, col_ld = swap ? d.lda : d.ldb;
       const int64_t lane_bs = swap ? d.b_batch_stride : d.a_batch_stride;
       const int64_t col_bs = swap ? d.a_batch_stride : d.b_batch_stride;
-      if (!P.lane_mn)
+      if (depth > 1) {  // packed: one box per operand and K block covers `depth` batch entries
+        encode_map(&m.lane, lane_t, d.K, lane_rows, d.batch, lane_ld, lane_bs, 64, lrows, depth);
+        if (!P.col_mn)
+          encode_map(&m.col[0], col_t, d.K, col_rows, d.batch, col_ld, col_bs, 64,
+                     static_cast<uint32_t>(round_up(col_rows, 16)), depth);
+        else
+          encode_map(&m.col[0], col_t, col_rows, d.K, d.batch, col_ld, col_bs, 64, 64, depth);
+      } else if (!P.lane_mn) {
         encode_map(&m.lane, lane_t, d.K, lane_rows, d.batch, lane_ld, lane_bs, 64, kLaneRows);
-      else
-        encode_map(&m.lane, lane_t, lane_rows, d.K, d.batch, lane_ld, lane_bs, 64, 64);
-      if (!P.col_mn) {
-        for (int q = 0; q < kColMaps; ++q)
-          encode_map(&m.col[q], col_t, d.K, col_rows, d.batch, col_ld, col_bs, 64, 256u >> q);
       } else {
-        encode_map(&m.col[0], col_t, col_rows, d.K, d.batch, col_ld, col_bs, 64, 64);
+        encode_map(&m.lane, lane_t, lane_rows, d.K, d.batch, lane_ld, lane_bs, 64, 64);
+      }
+      if (depth == 1) {
+        if (!P.col_mn) {
+          for (int q = 0; q < kColMaps; ++q)
+            encode_map(&m.col[q], col_t, d.K, col_rows, d.batch, col_ld, col_bs, 64, 256u >> q);
+        } else {
+          encode_map(&m.col[0], col_t, col_rows, d.K, d.batch, col_ld, col_bs, 64, 64);
+        }
       }
       ex.tma_out.push_back(encode_out_map(&m.out, d) ? 1 : 0);
       ex.maps.push_back(m);
@@ -433,6 +472,41 @@ static void upload(ExecImpl& I) {
     if (paired[i]) continue;
     const DevWork& w = I.work[i];
     const DevProblem& P = I.problems[w.problem];
+    const int32_t depth = I.pack_depth[w.problem];
+    if (depth > 1) {
+      // consecutive entries of the same piece shape -> one packed item
+      size_t j = i + 1;
+      while (j < I.work.size() && static_cast<int32_t>(j - i) < depth) {
+        const DevWork& u = I.work[j];
+        if (paired[j] || u.problem != w.problem || u.batch != w.batch + static_cast<int32_t>(j - i) ||
+            u.lane0 != w.lane0 || u.col0 != w.col0 || u.lane_len != w.lane_len || u.col_len != w.col_len)
+          break;
+        ++j;
+      }
+      const int32_t nb = static_cast<int32_t>(j - i);
+      bool ok = true;
+      for (size_t q = i; q < j; ++q) ok = ok && tma_ok(I.work[q]);
+      TcWork t;
+      std::memset(&t, 0, sizeof(t));
+      t.maps = I.d_maps + w.problem;
+      t.C = c_of(P, w.batch);
+      t.ldc = P.ldc;
+      t.lane0 = w.lane0;
+      t.col0 = w.col0;
+      t.lane_len = w.lane_len;
+      t.col_len = w.col_len;
+      t.n_mma = w.n_mma;
+      t.num_kb = P.num_kb;
+      t.batch = w.batch;
+      t.flags = flags_of(P) | (ok ? kFlagTmaStore : 0u);
+      t.pack = static_cast<uint32_t>(nb) | (static_cast<uint32_t>(depth) << 8) |
+               (static_cast<uint32_t>(I.pack_rows[w.problem]) << 16);
+      t.c_bs = static_cast<int32_t>(P.c_bs);
+      max_n = std::max(max_n, static_cast<int>(depth * round_up(w.n_mma, 32)));
+      tw.push_back(t);
+      i = j - 1;
+      continue;
+    }
     TcWork t;
     std::memset(&t, 0, sizeof(t));
     t.maps = I.d_maps + w.problem;

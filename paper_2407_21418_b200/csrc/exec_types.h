@@ -65,6 +65,12 @@ struct alignas(16) DevWork {
 //   at the tensor edge, so the epilogue may store through TMA (clipped by the
 //   hardware) instead of predicated st.global.
 enum : uint32_t { kFlagSwap = 1u, kFlagLaneMN = 2u, kFlagColMN = 4u, kFlagOutF32 = 8u, kFlagTmaStore = 16u };
+// Batch packing (BMM with one work piece per batch entry): `pack` holds
+// nb (entries in this item, bits 0-7), the problem's TMA box depth nb_max
+// (bits 8-15) and the lane box rows (bits 16-31); entry e of the item is batch
+// `batch + e`, staged at lane/col offsets e*lane_rows*128 / e*n_mma*128 in the
+// ring and accumulated at TMEM column e*round_up(n_mma, 32). pack == 0: a plain
+// single-entry item.
 struct alignas(64) TcWork {
   const DevMaps* maps;
   void* C;            // element 0 of this batch entry's output matrix
@@ -74,8 +80,13 @@ struct alignas(64) TcWork {
   int32_t n_mma, num_kb;
   int32_t batch;
   uint32_t flags;
-  int32_t pad_[2];
+  uint32_t pack;
+  int32_t c_bs;       // batch stride of C in elements (packed items)
 };
+__host__ __device__ inline int pack_nb(uint32_t p) { return p ? static_cast<int>(p & 0xFFu) : 1; }
+__host__ __device__ inline int pack_depth(uint32_t p) { return static_cast<int>((p >> 8) & 0xFFu); }
+__host__ __device__ inline int pack_lane_rows(uint32_t p) { return static_cast<int>(p >> 16); }
+constexpr int kMaxPack = 4;
 
 // CTA-pair work item (64 B): two 128-lane slabs (one per CTA of a cluster
 // pair) that share the column operand; N = n_mma columns, each CTA stages

@@ -136,7 +136,10 @@ __global__ void __launch_bounds__(kTcThreads, 1)
       }
       const CUtensorMap* tl = &it.maps->lane;
       const bool lane_mn = it.flags & kFlagLaneMN, col_mn = it.flags & kFlagColMN;
-      const uint32_t bytes = kLaneStageBytes + static_cast<uint32_t>(it.n_mma) * kBlockK * 2;
+      const int depth = pack_depth(it.pack);  // 0: not packed
+      const uint32_t bytes =
+          depth ? static_cast<uint32_t>(depth * (pack_lane_rows(it.pack) + it.n_mma) * kBlockK * 2)
+                : kLaneStageBytes + static_cast<uint32_t>(it.n_mma) * kBlockK * 2;
       const uint32_t cmask = col_box_mask(it.n_mma);
       int boff[kColMaps];  // smem row offset of each column box (widest first)
       {
@@ -169,13 +172,18 @@ __global__ void __launch_bounds__(kTcThreads, 1)
           uint8_t* ldst = lane_buf + s * kLaneStageBytes;
           uint8_t* cdst = col_buf + s * cfg.col_stage_bytes;
           const int k0 = kb * kBlockK;
-          if (!lane_mn) {
+          if (depth) {  // packed batch entries: one 3-D box per operand
+            tma_load_3d(ldst, tl, &full[s], k0, it.lane0, it.batch);
+            if (!col_mn) tma_load_3d(cdst, &it.maps->col[0], &full[s], k0, it.col0, it.batch);
+            else tma_load_3d(cdst, &it.maps->col[0], &full[s], it.col0, k0, it.batch);
+          } else if (!lane_mn) {
             tma_load_3d(ldst, tl, &full[s], k0, it.lane0, it.batch);
           } else {
             tma_load_3d(ldst, tl, &full[s], it.lane0, k0, it.batch);
             tma_load_3d(ldst + 8192, tl, &full[s], it.lane0 + 64, k0, it.batch);
           }
-          if (!col_mn) {
+          if (depth) {
+          } else if (!col_mn) {
 #pragma unroll
             for (int q = 0; q < kColMaps; ++q)
               if (cmask & (1u << q))
@@ -212,23 +220,43 @@ __global__ void __launch_bounds__(kTcThreads, 1)
     uint32_t ms = 0, mphase = 0;  // MMA ring slot / phase
     uint32_t local = 0;
     uint32_t pend = 0;
+#ifdef FTB_PROD_PROFILE
+    unsigned long long m_te = 0, m_full = 0, m_issue = 0, m_t0 = clock64();
+#endif
     if (static_cast<int>(blockIdx.x) < n_work) pend = fetch_work_word(work, blockIdx.x);
     for (int w = blockIdx.x; w < n_work; w += G, ++local) {
       const TcWork it = bcast_work(pend);
       if (w + G < n_work) pend = fetch_work_word(work, w + G);  // lands while this item runs
-      const uint32_t slot = local % cfg.n_acc;
-      const uint32_t use = local / cfg.n_acc;
       const uint32_t lane_mn = (it.flags & kFlagLaneMN) ? 1u : 0u;
       const uint32_t col_mn = (it.flags & kFlagColMN) ? 1u : 0u;
+      const uint32_t slot = local % cfg.n_acc;
+      const uint32_t use = local / cfg.n_acc;
+#ifdef FTB_PROD_PROFILE
+      unsigned long long mt0 = clock64();
+#endif
       mbar_wait(&tempty[slot], (use & 1) ^ 1);
       tc_fence_after();
+#ifdef FTB_PROD_PROFILE
+      m_te += clock64() - mt0;
+#endif
       const uint32_t tmem_d = tmem_base + slot * cfg.acc_cols;
       const uint32_t idesc = idesc_bf16_f32(kLaneRows, static_cast<uint32_t>(it.n_mma), lane_mn, col_mn);
+      const int nb = pack_nb(it.pack);
+      const uint32_t lane_step = it.pack ? static_cast<uint32_t>(pack_lane_rows(it.pack)) * 128u : 0u;
+      const uint32_t col_step = static_cast<uint32_t>(it.n_mma) * 128u;
+      const uint32_t acc_step = static_cast<uint32_t>((it.n_mma + 31) & ~31);
       for (int kb = 0; kb < it.num_kb; ++kb, ++g) {
         const uint32_t s = ms;
+#ifdef FTB_PROD_PROFILE
+        unsigned long long mf0 = clock64();
+#endif
         mbar_wait(&full[s], mphase);
         if (++ms == S) { ms = 0; mphase ^= 1; }
         tc_fence_after();
+#ifdef FTB_PROD_PROFILE
+        unsigned long long mf1 = clock64();
+        m_full += mf1 - mf0;
+#endif
         if (lane == 0) {
           if (kb == 0) trace_ev(cfg, local, 2);
 #ifndef FTB_TRACE_ISSUE
@@ -236,17 +264,23 @@ __global__ void __launch_bounds__(kTcThreads, 1)
 #endif
           const uint32_t la = smem_addr(lane_buf + s * kLaneStageBytes);
           const uint32_t ca = smem_addr(col_buf + s * cfg.col_stage_bytes);
+          for (int e = 0; e < nb; ++e) {  // packed batch entries (nb = 1 otherwise)
+            const uint32_t lae = la + e * lane_step, cae = ca + e * col_step;
 #pragma unroll
-          for (int kk = 0; kk < kBlockK / 16; ++kk) {
-            const uint64_t adesc = lane_mn ? umma_desc_sw128(la + kk * 2048, 8192, 1024)
-                                           : umma_desc_sw128(la + kk * 32, 16, 1024);
-            const uint64_t bdesc = col_mn ? umma_desc_sw128(ca + kk * 2048, 8192, 1024)
-                                          : umma_desc_sw128(ca + kk * 32, 16, 1024);
-            tc_mma_f16(tmem_d, adesc, bdesc, idesc, (kb | kk) != 0);
+            for (int kk = 0; kk < kBlockK / 16; ++kk) {
+              const uint64_t adesc = lane_mn ? umma_desc_sw128(lae + kk * 2048, 8192, 1024)
+                                             : umma_desc_sw128(lae + kk * 32, 16, 1024);
+              const uint64_t bdesc = col_mn ? umma_desc_sw128(cae + kk * 2048, 8192, 1024)
+                                            : umma_desc_sw128(cae + kk * 32, 16, 1024);
+              tc_mma_f16(tmem_d + e * acc_step, adesc, bdesc, idesc, (kb | kk) != 0);
+            }
           }
           tc_commit(&empty[s]);  // frees the smem slot when these MMAs finish
         }
         __syncwarp();
+#ifdef FTB_PROD_PROFILE
+        m_issue += clock64() - mf1;
+#endif
       }
       if (lane == 0) {
         tc_commit(&tfull[slot]);  // accumulator ready for the epilogue
@@ -254,6 +288,12 @@ __global__ void __launch_bounds__(kTcThreads, 1)
       }
       __syncwarp();
     }
+#ifdef FTB_PROD_PROFILE
+    if (lane == 0 && cfg.trace) {
+      unsigned long long* t = cfg.trace + static_cast<size_t>(blockIdx.x) * kTracePerCta;
+      t[6] = m_te; t[7] = m_full; t[8] = m_issue; t[9] = clock64() - m_t0;
+    }
+#endif
   } else {
     // ------------------------------------------------------------ epilogue
     const int quad = warp & 3;  // TMEM lane quadrant this warp may access
@@ -261,6 +301,9 @@ __global__ void __launch_bounds__(kTcThreads, 1)
     // two), or — for predicated items — the 32x33 fp32 transpose tile (aliased)
     uint8_t* region = reinterpret_cast<uint8_t*>(epi_buf) + quad * kEpiWarpBytes;
     uint32_t local = 0, ngrp = 0;
+#ifdef FTB_PROD_PROFILE
+    unsigned long long e_wait = 0, e_t0 = clock64();
+#endif
     TcWork nxt;
     if (static_cast<int>(blockIdx.x) < n_work) nxt = load_work(work, blockIdx.x);
     for (int w = blockIdx.x; w < n_work; w += G, ++local) {
@@ -270,21 +313,41 @@ __global__ void __launch_bounds__(kTcThreads, 1)
       const uint32_t use = local / cfg.n_acc;
       const bool swap = it.flags & kFlagSwap, f32 = it.flags & kFlagOutF32;
       const bool tma = it.flags & kFlagTmaStore;
+#ifdef FTB_PROD_PROFILE
+      unsigned long long ew0 = clock64();
+#endif
       mbar_wait(&tfull[slot], use & 1);
+#ifdef FTB_PROD_PROFILE
+      e_wait += clock64() - ew0;
+#endif
       tc_fence_after();
       if (quad == 0 && lane == 0) trace_ev(cfg, local, 4);
       const int lane_base = quad * 32;
       const uint32_t taddr = tmem_base + (static_cast<uint32_t>(lane_base) << 16) + slot * cfg.acc_cols;
-      epilogue_tile(region, ngrp, taddr, lane_base < it.lane_len, tma, swap, f32, &it.maps->out, it.C, it.ldc,
-                    it.lane0, it.lane_len, lane_base, it.col0, it.col_len, it.batch, [&] {
-                      tc_fence_before();
-                      __syncwarp();
-                      if (lane == 0) mbar_arrive(&tempty[slot]);
-                    });
+      const int nb = pack_nb(it.pack);
+      const uint32_t acc_step = static_cast<uint32_t>((it.n_mma + 31) & ~31);
+      const size_t c_step = static_cast<size_t>(it.c_bs) * (f32 ? 4 : 2);
+      for (int e = 0; e < nb; ++e) {  // packed batch entries (nb = 1 otherwise)
+        auto release = [&] {
+          if (e + 1 < nb) return;  // the slot is free after the last entry's TMEM reads
+          tc_fence_before();
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&tempty[slot]);
+        };
+        epilogue_tile(region, ngrp, taddr + e * acc_step, lane_base < it.lane_len, tma, swap, f32, &it.maps->out,
+                      static_cast<char*>(it.C) + e * c_step, it.ldc, it.lane0, it.lane_len, lane_base, it.col0,
+                      it.col_len, it.batch + e, release);
+      }
       if (quad == 0 && lane == 0) trace_ev(cfg, local, 5);
     }
     if (lane == 0) bulk_wait_all();  // output stores complete before the CTA retires
     __syncwarp();
+#ifdef FTB_PROD_PROFILE
+    if (lane == 0 && warp == 2 && cfg.trace) {
+      unsigned long long* t = cfg.trace + static_cast<size_t>(blockIdx.x) * kTracePerCta;
+      t[10] = e_wait; t[11] = clock64() - e_t0;
+    }
+#endif
   }
 
   tc_fence_before();

@@ -103,8 +103,12 @@ def test_dense_f32_out(cuda, b_layout):
 
 @pytest.mark.parametrize("T", [1, 5, 37, 64, 128])
 @pytest.mark.parametrize("kind", ["scores", "context"])
-def test_bmm_bf16(cuda, T, kind):
-    b = 6
+@pytest.mark.parametrize("b,pack", [(6, True), (9, True), (6, False)])
+def test_bmm_bf16(cuda, T, kind, b, pack, monkeypatch):
+    """BMM attention shapes; with packing, up to 4 consecutive batch entries
+    share one work item and one 3-D TMA box per operand (last group ragged)."""
+    if not pack:
+        monkeypatch.setenv("FTB_NO_PACK", "1")
     g = torch.Generator().manual_seed(T)
     if kind == "scores":
         # Q [b,T,64] @ K^T: B given as K [b, T(j), 64(k)] -> "nk" layout
