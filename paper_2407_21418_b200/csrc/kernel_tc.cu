@@ -105,6 +105,12 @@ __global__ void __launch_bounds__(kTcThreads, 1)
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_holder;
+  // Programmatic dependent launch: everything above (barrier init, TMEM
+  // allocation) overlaps the previous grid's tail; operands and outputs are
+  // touched only after it has completed. Dependents may launch right away —
+  // they in turn wait here for this grid.
+  griddep_wait();
+  griddep_launch_dependents();
   const int G = gridDim.x;
 
   if (warp == 0) {
@@ -372,8 +378,7 @@ static cudaError_t launch_tc_s(const TcWork* work, int32_t n_work, int32_t n_cta
     if (e != cudaSuccess) return e;
     configured = true;
   }
-  ftb_tc_kernel<S><<<n_ctas, kTcThreads, tc_smem_bytes(cfg), stream>>>(work, n_work, cfg);
-  return cudaGetLastError();
+  return launch_pdl(ftb_tc_kernel<S>, n_ctas, kTcThreads, tc_smem_bytes(cfg), stream, work, n_work, cfg);
 }
 
 cudaError_t launch_tc(const TcWork* work, int32_t n_work, int32_t n_ctas, TcConfig cfg,

@@ -59,6 +59,12 @@ __device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* m, uin
       : "memory");
 }
 
+// ---------------------------------------------------------------- programmatic dependent launch
+__device__ __forceinline__ void griddep_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void griddep_launch_dependents() {
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
+
 // ---------------------------------------------------------------- tcgen05
 template <int kCols>
 __device__ __forceinline__ void tmem_alloc(uint32_t* holder_smem) {
@@ -218,5 +224,31 @@ __device__ __forceinline__ void tc_commit_pair_mc(uint64_t* bar) {
           smem_addr(bar)),
       "h"(mask)
       : "memory");
+}
+}  // namespace ftb
+
+#include <cstdlib>
+#include <cuda_runtime.h>
+namespace ftb {
+// Launch with programmatic stream serialization (PDL) unless FTB_PDL=0: the
+// kernel's prologue may overlap the previous kernel's tail on the stream.
+template <typename... KArgs, typename... Args>
+inline cudaError_t launch_pdl(void (*kernel)(KArgs...), int grid, int block, int smem, cudaStream_t stream,
+                              Args... args) {
+  static const bool pdl = [] {
+    const char* e = std::getenv("FTB_PDL");
+    return !(e && e[0] == '0');
+  }();
+  cudaLaunchConfig_t lc = {};
+  lc.gridDim = dim3(static_cast<unsigned>(grid));
+  lc.blockDim = dim3(static_cast<unsigned>(block));
+  lc.dynamicSmemBytes = static_cast<size_t>(smem);
+  lc.stream = stream;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  lc.attrs = at;
+  lc.numAttrs = pdl ? 1 : 0;
+  return cudaLaunchKernelEx(&lc, kernel, args...);
 }
 }  // namespace ftb
