@@ -283,29 +283,27 @@ static void build(ExecImpl& ex, const ftb_gemm_desc* probs, const ftb_program* p
     P.lane_mn = swap && !P.b_nk;
     P.col_mn = !swap && !P.b_nk;
     if (!ffma && d.in_dtype != FTB_DT_BF16) throw input_error("unsupported input dtype", "in_dtype");
-    // Batch packing: a BMM whose every batch entry is one work piece (lane
-    // extent <= 128, column extent <= 256, K-major lane operand, and a column
-    // operand that is K-major or a single 64-wide MN-major box) runs up to
-    // kMaxPack consecutive entries per work item, loaded by one 3-D TMA box per
-    // operand and K block (the box's third dimension is the batch).
+    // Block-diagonal batch packing for short attention BMMs: when every
+    // batch entry is one work piece with M <= 64 rows and N <= 64 columns,
+    // `depth` = 128 / lane_slot consecutive entries share one work item. One
+    // 3-D TMA box per operand and K block stacks entry e's A rows at lanes
+    // [e*lane_slot, ...) and its B rows at MMA columns [e*64, ...); a single
+    // M=128, N=depth*64 MMA computes every entry's block (and the unused
+    // off-diagonal blocks: a kind::f16 MMA costs ~100 clk whatever N <= 128
+    // is, so one N=256 MMA replaces four N=64 ones at a third of the tensor
+    // time), and each epilogue warp drains the diagonal block in its TMEM lane
+    // quadrant. The box's third dimension is the batch; rows/columns past M,
+    // N and past the last batch entry are zero-filled by TMA.
     int32_t depth = 1, lrows = 0;
-    if (!ffma && d.op == FTB_OP_BMM && !P.lane_mn) {
-      const int64_t lane_ext = swap ? d.N : d.M, col_ext = swap ? d.M : d.N;
+    if (!ffma && d.op == FTB_OP_BMM && !swap && !P.lane_mn && d.M <= 64 && d.N <= 64) {
       bool one_piece = true;
-      for (const Region& r : regs) {
-        const int64_t li = r.hi[ib] - r.lo[ib], lj = r.hi[ib + 1] - r.lo[ib + 1];
-        if ((swap ? lj : li) != lane_ext || (swap ? li : lj) != col_ext) one_piece = false;
-      }
-      const int64_t ncols = P.col_mn ? 64 : round_up(col_ext, 16);
-      if (one_piece && lane_ext <= kLaneRows && (!P.col_mn || col_ext <= 64) && ncols <= kMaxN) {
-        lrows = static_cast<int32_t>(round_up(lane_ext, 16));
-        const int64_t cstride = round_up(ncols, 32);
-        const char* pm = std::getenv("FTB_PACK_MAX");
-        const int64_t pack_max = pm ? std::max(1, std::min(kMaxPack, std::atoi(pm))) : kMaxPack;
-        int64_t nb = std::min<int64_t>({pack_max, kLaneRows / lrows, kMaxN / ncols, kMaxN / cstride,
-                                        static_cast<int64_t>(d.batch)});
-        const int64_t c_bs = d.c_batch_stride;
-        if (nb >= 2 && c_bs < (int64_t(1) << 31) && !std::getenv("FTB_NO_PACK")) depth = static_cast<int32_t>(nb);
+      for (const Region& r : regs)
+        if (r.hi[ib] - r.lo[ib] != d.M || r.hi[ib + 1] - r.lo[ib + 1] != d.N) one_piece = false;
+      const int32_t slot_rows = d.M <= 32 ? 32 : 64;
+      const int32_t nb = std::min<int32_t>(kLaneRows / slot_rows, d.batch);
+      if (one_piece && nb >= 2 && d.c_batch_stride < (int64_t(1) << 31) && !std::getenv("FTB_NO_PACK")) {
+        depth = kLaneRows / slot_rows;
+        lrows = slot_rows;
       }
     }
     ex.pack_depth.push_back(depth);
@@ -323,8 +321,7 @@ static void build(ExecImpl& ex, const ftb_gemm_desc* probs, const ftb_program* p
       if (depth > 1) {  // packed: one box per operand and K block covers `depth` batch entries
         encode_map(&m.lane, lane_t, d.K, lane_rows, d.batch, lane_ld, lane_bs, 64, lrows, depth);
         if (!P.col_mn)
-          encode_map(&m.col[0], col_t, d.K, col_rows, d.batch, col_ld, col_bs, 64,
-                     static_cast<uint32_t>(round_up(col_rows, 16)), depth);
+          encode_map(&m.col[0], col_t, d.K, col_rows, d.batch, col_ld, col_bs, 64, 64, depth);
         else
           encode_map(&m.col[0], col_t, col_rows, d.K, d.batch, col_ld, col_bs, 64, 64, depth);
       } else if (!P.lane_mn) {
@@ -495,14 +492,14 @@ static void upload(ExecImpl& I) {
       t.col0 = w.col0;
       t.lane_len = w.lane_len;
       t.col_len = w.col_len;
-      t.n_mma = w.n_mma;
+      t.n_mma = depth * 64;  // the whole stacked MMA (entry e in columns [64e, 64e + 64))
       t.num_kb = P.num_kb;
       t.batch = w.batch;
       t.flags = flags_of(P) | (ok ? kFlagTmaStore : 0u);
       t.pack = static_cast<uint32_t>(nb) | (static_cast<uint32_t>(depth) << 8) |
                (static_cast<uint32_t>(I.pack_rows[w.problem]) << 16);
       t.c_bs = static_cast<int32_t>(P.c_bs);
-      max_n = std::max(max_n, static_cast<int>(depth * round_up(w.n_mma, 32)));
+      max_n = std::max(max_n, t.n_mma);
       tw.push_back(t);
       i = j - 1;
       continue;

@@ -65,12 +65,11 @@ struct alignas(16) DevWork {
 //   at the tensor edge, so the epilogue may store through TMA (clipped by the
 //   hardware) instead of predicated st.global.
 enum : uint32_t { kFlagSwap = 1u, kFlagLaneMN = 2u, kFlagColMN = 4u, kFlagOutF32 = 8u, kFlagTmaStore = 16u };
-// Batch packing (BMM with one work piece per batch entry): `pack` holds
-// nb (entries in this item, bits 0-7), the problem's TMA box depth nb_max
-// (bits 8-15) and the lane box rows (bits 16-31); entry e of the item is batch
-// `batch + e`, staged at lane/col offsets e*lane_rows*128 / e*n_mma*128 in the
-// ring and accumulated at TMEM column e*round_up(n_mma, 32). pack == 0: a plain
-// single-entry item.
+// Block-diagonal batch packing (short attention BMMs, exec.cu): `pack` holds
+// nb (entries in this item, bits 0-7), the TMA box depth (bits 8-15) and the
+// lane slot rows (32 or 64, bits 16-31); entry e of the item is batch
+// `batch + e`, its A rows sit at lanes [e*slot, (e+1)*slot) and its result in
+// TMEM columns [64e, 64e + 64) of those lanes. pack == 0: a plain item.
 struct alignas(64) TcWork {
   const DevMaps* maps;
   void* C;            // element 0 of this batch entry's output matrix

@@ -144,7 +144,7 @@ __global__ void __launch_bounds__(kTcThreads, 1)
       const bool lane_mn = it.flags & kFlagLaneMN, col_mn = it.flags & kFlagColMN;
       const int depth = pack_depth(it.pack);  // 0: not packed
       const uint32_t bytes =
-          depth ? static_cast<uint32_t>(depth * (pack_lane_rows(it.pack) + it.n_mma) * kBlockK * 2)
+          depth ? static_cast<uint32_t>(depth * (pack_lane_rows(it.pack) + 64) * kBlockK * 2)
                 : kLaneStageBytes + static_cast<uint32_t>(it.n_mma) * kBlockK * 2;
       const uint32_t cmask = col_box_mask(it.n_mma);
       int boff[kColMaps];  // smem row offset of each column box (widest first)
@@ -247,10 +247,6 @@ __global__ void __launch_bounds__(kTcThreads, 1)
 #endif
       const uint32_t tmem_d = tmem_base + slot * cfg.acc_cols;
       const uint32_t idesc = idesc_bf16_f32(kLaneRows, static_cast<uint32_t>(it.n_mma), lane_mn, col_mn);
-      const int nb = pack_nb(it.pack);
-      const uint32_t lane_step = it.pack ? static_cast<uint32_t>(pack_lane_rows(it.pack)) * 128u : 0u;
-      const uint32_t col_step = static_cast<uint32_t>(it.n_mma) * 128u;
-      const uint32_t acc_step = static_cast<uint32_t>((it.n_mma + 31) & ~31);
       for (int kb = 0; kb < it.num_kb; ++kb, ++g) {
         const uint32_t s = ms;
 #ifdef FTB_PROD_PROFILE
@@ -270,16 +266,13 @@ __global__ void __launch_bounds__(kTcThreads, 1)
 #endif
           const uint32_t la = smem_addr(lane_buf + s * kLaneStageBytes);
           const uint32_t ca = smem_addr(col_buf + s * cfg.col_stage_bytes);
-          for (int e = 0; e < nb; ++e) {  // packed batch entries (nb = 1 otherwise)
-            const uint32_t lae = la + e * lane_step, cae = ca + e * col_step;
 #pragma unroll
-            for (int kk = 0; kk < kBlockK / 16; ++kk) {
-              const uint64_t adesc = lane_mn ? umma_desc_sw128(lae + kk * 2048, 8192, 1024)
-                                             : umma_desc_sw128(lae + kk * 32, 16, 1024);
-              const uint64_t bdesc = col_mn ? umma_desc_sw128(cae + kk * 2048, 8192, 1024)
-                                            : umma_desc_sw128(cae + kk * 32, 16, 1024);
-              tc_mma_f16(tmem_d + e * acc_step, adesc, bdesc, idesc, (kb | kk) != 0);
-            }
+          for (int kk = 0; kk < kBlockK / 16; ++kk) {
+            const uint64_t adesc = lane_mn ? umma_desc_sw128(la + kk * 2048, 8192, 1024)
+                                           : umma_desc_sw128(la + kk * 32, 16, 1024);
+            const uint64_t bdesc = col_mn ? umma_desc_sw128(ca + kk * 2048, 8192, 1024)
+                                          : umma_desc_sw128(ca + kk * 32, 16, 1024);
+            tc_mma_f16(tmem_d, adesc, bdesc, idesc, (kb | kk) != 0);
           }
           tc_commit(&empty[s]);  // frees the smem slot when these MMAs finish
         }
@@ -330,19 +323,22 @@ __global__ void __launch_bounds__(kTcThreads, 1)
       if (quad == 0 && lane == 0) trace_ev(cfg, local, 4);
       const int lane_base = quad * 32;
       const uint32_t taddr = tmem_base + (static_cast<uint32_t>(lane_base) << 16) + slot * cfg.acc_cols;
-      const int nb = pack_nb(it.pack);
-      const uint32_t acc_step = static_cast<uint32_t>((it.n_mma + 31) & ~31);
-      const size_t c_step = static_cast<size_t>(it.c_bs) * (f32 ? 4 : 2);
-      for (int e = 0; e < nb; ++e) {  // packed batch entries (nb = 1 otherwise)
-        auto release = [&] {
-          if (e + 1 < nb) return;  // the slot is free after the last entry's TMEM reads
-          tc_fence_before();
-          __syncwarp();
-          if (lane == 0) mbar_arrive(&tempty[slot]);
-        };
-        epilogue_tile(region, ngrp, taddr + e * acc_step, lane_base < it.lane_len, tma, swap, f32, &it.maps->out,
-                      static_cast<char*>(it.C) + e * c_step, it.ldc, it.lane0, it.lane_len, lane_base, it.col0,
-                      it.col_len, it.batch + e, release);
+      auto release = [&] {
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&tempty[slot]);
+      };
+      if (!it.pack) {
+        epilogue_tile(region, ngrp, taddr, lane_base < it.lane_len, tma, swap, f32, &it.maps->out, it.C, it.ldc,
+                      it.lane0, it.lane_len, lane_base, it.col0, it.col_len, it.batch, release);
+      } else {
+        // block-diagonal pack: this warp's lane quadrant belongs to entry e
+        const int wpe = pack_lane_rows(it.pack) / 32;  // warps per entry
+        const int e = quad / wpe, r0 = (quad % wpe) * 32;
+        const bool active = e < pack_nb(it.pack) && r0 < it.lane_len;
+        epilogue_tile(region, ngrp, taddr + e * 64, active, tma, swap, f32, &it.maps->out,
+                      static_cast<char*>(it.C) + static_cast<size_t>(e) * it.c_bs * (f32 ? 4 : 2), it.ldc, 0,
+                      it.lane_len, r0, 0, it.col_len, it.batch + e, release);
       }
       if (quad == 0 && lane == 0) trace_ev(cfg, local, 5);
     }
