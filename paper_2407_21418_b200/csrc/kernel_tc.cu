@@ -104,7 +104,9 @@ __global__ void __launch_bounds__(kTcThreads, 1)
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
-  const uint32_t tmem_base = *tmem_holder;
+  const uint32_t tmem_base = __shfl_sync(0xffffffffu, *tmem_holder, 0);  // warp-uniform
+  const uint32_t smem_u32 = smem_addr(smem);
+  const uint32_t lane_u32 = smem_addr(lane_buf), col_u32 = smem_addr(col_buf);
   // Programmatic dependent launch: everything above (barrier init, TMEM
   // allocation) overlaps the previous grid's tail; operands and outputs are
   // touched only after it has completed. Dependents may launch right away —
@@ -171,9 +173,8 @@ __global__ void __launch_bounds__(kTcThreads, 1)
         c_wait += cs - cw;
 #endif
         if (lane == 0) {
-#ifdef FTB_TRACE_ISSUE
-          trace_kb(cfg, g, 1);  // debug: time before the TMA issue (replaces "MMA saw data")
-#endif
+          // one lane issues: measured faster here than the converged elect form
+          // (619 vs 504 clk per K block, scripts/prod_profile.py)
           mbar_arrive_expect_tx(&full[s], bytes);
           uint8_t* ldst = lane_buf + s * kLaneStageBytes;
           uint8_t* cdst = col_buf + s * cfg.col_stage_bytes;
@@ -182,21 +183,22 @@ __global__ void __launch_bounds__(kTcThreads, 1)
             tma_load_3d(ldst, tl, &full[s], k0, it.lane0, it.batch);
             if (!col_mn) tma_load_3d(cdst, &it.maps->col[0], &full[s], k0, it.col0, it.batch);
             else tma_load_3d(cdst, &it.maps->col[0], &full[s], it.col0, k0, it.batch);
-          } else if (!lane_mn) {
-            tma_load_3d(ldst, tl, &full[s], k0, it.lane0, it.batch);
           } else {
-            tma_load_3d(ldst, tl, &full[s], it.lane0, k0, it.batch);
-            tma_load_3d(ldst + 8192, tl, &full[s], it.lane0 + 64, k0, it.batch);
-          }
-          if (depth) {
-          } else if (!col_mn) {
+            if (!lane_mn) {
+              tma_load_3d(ldst, tl, &full[s], k0, it.lane0, it.batch);
+            } else {
+              tma_load_3d(ldst, tl, &full[s], it.lane0, k0, it.batch);
+              tma_load_3d(ldst + 8192, tl, &full[s], it.lane0 + 64, k0, it.batch);
+            }
+            if (!col_mn) {
 #pragma unroll
-            for (int q = 0; q < kColMaps; ++q)
-              if (cmask & (1u << q))
-                tma_load_3d(cdst + boff[q] * 128, &it.maps->col[q], &full[s], k0, it.col0 + boff[q], it.batch);
-          } else {
-            for (int c = 0; c < it.n_mma; c += 64)
-              tma_load_3d(cdst + c * 128, &it.maps->col[0], &full[s], it.col0 + c, k0, it.batch);
+              for (int q = 0; q < kColMaps; ++q)
+                if (cmask & (1u << q))
+                  tma_load_3d(cdst + boff[q] * 128, &it.maps->col[q], &full[s], k0, it.col0 + boff[q], it.batch);
+            } else {
+              for (int c = 0; c < it.n_mma; c += 64)
+                tma_load_3d(cdst + c * 128, &it.maps->col[0], &full[s], it.col0 + c, k0, it.batch);
+            }
           }
           if (kb == 0) trace_ev(cfg, local, 1);
           trace_kb(cfg, g, 0);
@@ -264,27 +266,27 @@ __global__ void __launch_bounds__(kTcThreads, 1)
 #ifndef FTB_TRACE_ISSUE
           trace_kb(cfg, g, 1);
 #endif
-          const uint32_t la = smem_addr(lane_buf + s * kLaneStageBytes);
-          const uint32_t ca = smem_addr(col_buf + s * cfg.col_stage_bytes);
+        }
+        {
+          const uint32_t la = lane_u32 + s * kLaneStageBytes;
+          const uint32_t ca = col_u32 + s * static_cast<uint32_t>(cfg.col_stage_bytes);
 #pragma unroll
           for (int kk = 0; kk < kBlockK / 16; ++kk) {
             const uint64_t adesc = lane_mn ? umma_desc_sw128(la + kk * 2048, 8192, 1024)
                                            : umma_desc_sw128(la + kk * 32, 16, 1024);
             const uint64_t bdesc = col_mn ? umma_desc_sw128(ca + kk * 2048, 8192, 1024)
                                           : umma_desc_sw128(ca + kk * 32, 16, 1024);
-            tc_mma_f16(tmem_d, adesc, bdesc, idesc, (kb | kk) != 0);
+            tc_mma_f16_elect(tmem_d, adesc, bdesc, idesc, (kb | kk) != 0);
           }
-          tc_commit(&empty[s]);  // frees the smem slot when these MMAs finish
+          tc_commit_elect(smem_u32 + static_cast<uint32_t>(reinterpret_cast<uint8_t*>(&empty[s]) - smem));
         }
         __syncwarp();
 #ifdef FTB_PROD_PROFILE
         m_issue += clock64() - mf1;
 #endif
       }
-      if (lane == 0) {
-        tc_commit(&tfull[slot]);  // accumulator ready for the epilogue
-        trace_ev(cfg, local, 3);
-      }
+      tc_commit_elect(smem_u32 + static_cast<uint32_t>(reinterpret_cast<uint8_t*>(&tfull[slot]) - smem));
+      if (lane == 0) trace_ev(cfg, local, 3);  // accumulator ready for the epilogue
       __syncwarp();
     }
 #ifdef FTB_PROD_PROFILE
