@@ -83,53 +83,65 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kTcThreads, 1)
   cluster_sync();  // barriers of both CTAs initialised, TMEM allocated on both
   tc_fence_after();
   const uint32_t tmem_base = *tmem_holder;
+  griddep_wait();  // operands / outputs only after the previous grid (PDL)
+  griddep_launch_dependents();
   const int G = gridDim.x >> 1;          // clusters
   const int cid = blockIdx.x >> 1;       // this cluster
 
   if (warp == 0) {
     // ------------------------------------------------------------ producer (both CTAs)
-    if (lane == 0) {
-      uint32_t g = 0;
-      uint32_t ps = 0, pphase = 0;  // producer ring slot / phase
-      uint32_t local = 0;
+    // whole warp walks the loops (records fetched ahead, broadcast with shfl);
+    // lane 0 arms the leader's barrier (leader CTA) and issues the 2-SM loads
+    uint32_t g = 0;
+    uint32_t ps = 0, pphase = 0;  // producer ring slot / phase
+    uint32_t local = 0;
 #ifdef FTB_PROD_PROFILE
-      unsigned long long c_wait = 0, c_issue = 0, c_item = 0, c_t0 = clock64();
+    unsigned long long c_wait = 0, c_issue = 0, c_item = 0, c_t0 = clock64();
 #endif
-      TcPair nxt;
-      if (cid < n_work) nxt = load_pair(work, cid);
-      for (int w = cid; w < n_work; w += G, ++local) {
-        const TcPair it = nxt;
-        if (w + G < n_work) nxt = load_pair(work, w + G);
+    TcPair cur, nxt;
+    uint32_t pend = 0;
+    if (cid < n_work) cur = bcast_record<TcPair>(fetch_record_word(work, cid));
+    if (cid + G < n_work) nxt = bcast_record<TcPair>(fetch_record_word(work, cid + G));
+    if (cid + 2 * G < n_work) pend = fetch_record_word(work, cid + 2 * G);
+    for (int w = cid; w < n_work; w += G, ++local) {
+      const TcPair it = cur;
+      if (lane == 0) {
         trace2_ev(cfg, local, 0);
-#ifdef FTB_PROD_PROFILE
-        unsigned long long ci = clock64();
-#endif
-        const bool lane_mn = it.flags & kFlagLaneMN, col_mn = it.flags & kFlagColMN;
-        const int half = it.n_mma >> 1;
-        const int lane0 = rank ? it.lane0[1] : it.lane0[0];
-        const int colr = it.col0 + static_cast<int>(rank) * half;
-        const uint32_t bytes_cta = kLaneStageBytes + static_cast<uint32_t>(half) * kBlockK * 2;
-        const uint32_t cmask = col_box_mask(half);
-        int boff[kColMaps];  // smem row offset of each column box (widest first)
-        {
-          int r = 0;
-#pragma unroll
-          for (int q = 0; q < kColMaps; ++q) {
-            boff[q] = r;
-            if (cmask & (1u << q)) r += 256 >> q;
-          }
+        if (w + G < n_work) {
+          tma_prefetch_desc(&nxt.maps->lane);
+          tma_prefetch_desc(&nxt.maps->col[1]);
         }
-        for (int kb = 0; kb < it.num_kb; ++kb, ++g) {
-          const uint32_t s = ps;
+      }
 #ifdef FTB_PROD_PROFILE
-          unsigned long long cw = clock64();
+      unsigned long long ci = clock64();
 #endif
-          mbar_wait(&empty[s], pphase ^ 1);
-          if (++ps == S) { ps = 0; pphase ^= 1; }
+      const bool lane_mn = it.flags & kFlagLaneMN, col_mn = it.flags & kFlagColMN;
+      const int half = it.n_mma >> 1;
+      const int lane0 = rank ? it.lane0[1] : it.lane0[0];
+      const int colr = it.col0 + static_cast<int>(rank) * half;
+      const uint32_t bytes_cta = kLaneStageBytes + static_cast<uint32_t>(half) * kBlockK * 2;
+      const uint32_t cmask = col_box_mask(half);
+      int boff[kColMaps];  // smem row offset of each column box (widest first)
+      {
+        int r = 0;
+#pragma unroll
+        for (int q = 0; q < kColMaps; ++q) {
+          boff[q] = r;
+          if (cmask & (1u << q)) r += 256 >> q;
+        }
+      }
+      for (int kb = 0; kb < it.num_kb; ++kb, ++g) {
+        const uint32_t s = ps;
 #ifdef FTB_PROD_PROFILE
-          unsigned long long cs = clock64();
-          c_wait += cs - cw;
+        unsigned long long cw = clock64();
 #endif
+        mbar_wait(&empty[s], pphase ^ 1);
+        if (++ps == S) { ps = 0; pphase ^= 1; }
+#ifdef FTB_PROD_PROFILE
+        unsigned long long cs = clock64();
+        c_wait += cs - cw;
+#endif
+        if (lane == 0) {
           const uint32_t fb = smem_addr(&full[s]) & kPeerBitMask;  // leader's barrier
           if (leader) mbar_arrive_expect_tx(&full[s], 2 * bytes_cta);
           uint8_t* ldst = lane_buf + s * kLaneStageBytes;
@@ -152,61 +164,72 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kTcThreads, 1)
           }
           if (kb == 0) trace2_ev(cfg, local, 1);
           trace2_kb(cfg, g, 0);
-#ifdef FTB_PROD_PROFILE
-          c_issue += clock64() - cs;
-#endif
         }
+        __syncwarp();
 #ifdef FTB_PROD_PROFILE
-        c_item += clock64() - ci;
+        c_issue += clock64() - cs;
 #endif
       }
 #ifdef FTB_PROD_PROFILE
-      if (cfg.trace) {
-        unsigned long long* t = cfg.trace + static_cast<size_t>(blockIdx.x) * kTracePerCta;
-        t[0] = c_wait; t[1] = c_issue; t[2] = c_item; t[3] = g; t[4] = local; t[5] = clock64() - c_t0;
-      }
+      c_item += clock64() - ci;
 #endif
+      cur = nxt;
+      if (w + 2 * G < n_work) nxt = bcast_record<TcPair>(pend);
+      if (w + 3 * G < n_work) pend = fetch_record_word(work, w + 3 * G);
     }
+#ifdef FTB_PROD_PROFILE
+    if (lane == 0 && cfg.trace) {
+      unsigned long long* t = cfg.trace + static_cast<size_t>(blockIdx.x) * kTracePerCta;
+      t[0] = c_wait; t[1] = c_issue; t[2] = c_item; t[3] = g; t[4] = local; t[5] = clock64() - c_t0;
+    }
+#endif
   } else if (warp == 1) {
     // ------------------------------------------------------------ MMA issuer (leader)
-    if (leader && lane == 0) {
+    // whole warp walks the loops; tcgen05.mma / commits issued converged with elect.sync
+    if (leader) {
       uint32_t g = 0;
       uint32_t ms = 0, mphase = 0;  // MMA ring slot / phase
       uint32_t local = 0;
-      TcPair nxt;
-      if (cid < n_work) nxt = load_pair(work, cid);
+      uint32_t pend = 0;
+      const uint32_t tmem_u = __shfl_sync(0xffffffffu, tmem_base, 0);
+      const uint32_t lane_u32 = smem_addr(lane_buf), col_u32 = smem_addr(col_buf);
+      if (cid < n_work) pend = fetch_record_word(work, cid);
       for (int w = cid; w < n_work; w += G, ++local) {
-        const TcPair it = nxt;
-        if (w + G < n_work) nxt = load_pair(work, w + G);
+        const TcPair it = bcast_record<TcPair>(pend);
+        if (w + G < n_work) pend = fetch_record_word(work, w + G);
         const uint32_t slot = local % cfg.n_acc;
         const uint32_t use = local / cfg.n_acc;
         const uint32_t lane_mn = (it.flags & kFlagLaneMN) ? 1u : 0u;
         const uint32_t col_mn = (it.flags & kFlagColMN) ? 1u : 0u;
         mbar_wait(&tempty[slot], (use & 1) ^ 1);
         tc_fence_after();
-        const uint32_t tmem_d = tmem_base + slot * cfg.acc_cols;
+        const uint32_t tmem_d = tmem_u + slot * cfg.acc_cols;
         const uint32_t idesc = idesc_bf16_f32(2 * kLaneRows, static_cast<uint32_t>(it.n_mma), lane_mn, col_mn);
         for (int kb = 0; kb < it.num_kb; ++kb, ++g) {
           const uint32_t s = ms;
           mbar_wait(&full[s], mphase);
           if (++ms == S) { ms = 0; mphase ^= 1; }
           tc_fence_after();
-          if (kb == 0) trace2_ev(cfg, local, 2);
-          trace2_kb(cfg, g, 1);
-          const uint32_t la = smem_addr(lane_buf + s * kLaneStageBytes);
-          const uint32_t ca = smem_addr(col_buf + s * cfg.col_stage_bytes);
+          if (lane == 0) {
+            if (kb == 0) trace2_ev(cfg, local, 2);
+            trace2_kb(cfg, g, 1);
+          }
+          const uint32_t la = lane_u32 + s * kLaneStageBytes;
+          const uint32_t ca = col_u32 + s * static_cast<uint32_t>(cfg.col_stage_bytes);
 #pragma unroll
           for (int kk = 0; kk < kBlockK / 16; ++kk) {
             const uint64_t adesc = lane_mn ? umma_desc_sw128(la + kk * 2048, 8192, 1024)
                                            : umma_desc_sw128(la + kk * 32, 16, 1024);
             const uint64_t bdesc = col_mn ? umma_desc_sw128(ca + kk * 2048, 8192, 1024)
                                           : umma_desc_sw128(ca + kk * 32, 16, 1024);
-            tc_mma_f16_pair(tmem_d, adesc, bdesc, idesc, (kb | kk) != 0);
+            tc_mma_f16_pair_elect(tmem_d, adesc, bdesc, idesc, (kb | kk) != 0);
           }
-          tc_commit_pair_mc(&empty[s]);
+          tc_commit_pair_mc_elect(smem_addr(&empty[s]));
+          __syncwarp();
         }
-        tc_commit_pair_mc(&tfull[slot]);
-        trace2_ev(cfg, local, 3);
+        tc_commit_pair_mc_elect(smem_addr(&tfull[slot]));
+        if (lane == 0) trace2_ev(cfg, local, 3);
+        __syncwarp();
       }
     }
   } else {
@@ -218,7 +241,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kTcThreads, 1)
     if (cid < n_work) nxt = load_pair(work, cid);
     for (int w = cid; w < n_work; w += G, ++local) {
       const TcPair it = nxt;
-      if (w + G < n_work) nxt = load_pair(work, w + G);
+      if (w + G < n_work) nxt = load_pair(work, w + G);  // lands while this item runs
       const uint32_t slot = local % cfg.n_acc;
       const uint32_t use = local / cfg.n_acc;
       const bool swap = it.flags & kFlagSwap, f32 = it.flags & kFlagOutF32;
@@ -261,8 +284,7 @@ static cudaError_t launch_tc2_s(const TcPair* work, int32_t n_work, int32_t n_ct
     if (e != cudaSuccess) return e;
     configured = true;
   }
-  ftb_tc2_kernel<S><<<n_ctas, kTcThreads, tc_smem_bytes(cfg), stream>>>(work, n_work, cfg);
-  return cudaGetLastError();
+  return launch_pdl(ftb_tc2_kernel<S>, n_ctas, kTcThreads, tc_smem_bytes(cfg), stream, work, n_work, cfg);
 }
 
 cudaError_t launch_tc2(const TcPair* work, int32_t n_work, int32_t n_ctas, TcConfig cfg,

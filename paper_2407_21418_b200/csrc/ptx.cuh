@@ -96,6 +96,43 @@ __device__ __forceinline__ void tc_commit_elect(uint32_t bar) {
       : "memory");
 }
 
+__device__ __forceinline__ void tc_mma_f16_pair_elect(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc,
+                                                      uint32_t idesc, uint32_t accumulate) {
+  asm volatile(
+      "{\n.reg .pred p, q;\nelect.sync _|p, 0xffffffff;\n"
+      "setp.ne.b32 q, %4, 0;\n"
+      "@p tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, q;\n}\n" ::"r"(tmem_d),
+      "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate)
+      : "memory");
+}
+// arrive on `bar` (same smem offset) in both CTAs of the pair
+__device__ __forceinline__ void tc_commit_pair_mc_elect(uint32_t bar) {
+  asm volatile(
+      "{\n.reg .pred p;\nelect.sync _|p, 0xffffffff;\n"
+      "@p tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;\n}\n" ::"r"(
+          bar),
+      "h"(static_cast<uint16_t>(0x3))
+      : "memory");
+}
+
+// 64-B work records: each of lanes 0..15 loads one 32-bit word (a coalesced
+// load whose latency overlaps the current item), later broadcast with shfl
+// from constant lanes, which ptxas treats as warp-uniform. Warp converged.
+template <class T>
+__device__ __forceinline__ uint32_t fetch_record_word(const T* __restrict__ base, int w) {
+  static_assert(sizeof(T) == 64, "64-B records");
+  const int lane = threadIdx.x & 31;
+  return lane < 16 ? __ldg(reinterpret_cast<const uint32_t*>(base + w) + lane) : 0u;
+}
+template <class T>
+__device__ __forceinline__ T bcast_record(uint32_t mine) {
+  T it;
+  uint32_t* dst = reinterpret_cast<uint32_t*>(&it);
+#pragma unroll
+  for (int q = 0; q < 16; ++q) dst[q] = __shfl_sync(0xffffffffu, mine, q);
+  return it;
+}
+
 // ---------------------------------------------------------------- programmatic dependent launch
 __device__ __forceinline__ void griddep_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
 __device__ __forceinline__ void griddep_launch_dependents() {

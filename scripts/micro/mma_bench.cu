@@ -35,7 +35,7 @@ __global__ void __launch_bounds__(128, 1) mma_kernel(const __grid_constant__ Map
   const uint32_t tmem = *holder;
   __shared__ unsigned long long tiss[16], tland[16];
   unsigned long long t0 = clock64();
-  if (warp == 0 && lane == 0 && mma_on < 2) {
+  if (warp == 0 && lane == 0 && mma_on < 2) {  // (modes >= 2: no producer)
     int ps = 0, ph = 0;
     for (int it = 0; it < iters; ++it) {
       mbar_wait(&empty[ps], ph ^ 1);
@@ -55,6 +55,27 @@ __global__ void __launch_bounds__(128, 1) mma_kernel(const __grid_constant__ Map
       if (it < 16) tiss[it] = clock64() - t0;
       if (++ps == S) { ps = 0; ph ^= 1; }
     }
+  } else if (warp == 1 && mma_on == 7) {
+    const uint32_t tm = __shfl_sync(0xffffffffu, tmem, 0);
+    const uint32_t idesc = idesc_bf16_f32(PAIR ? 256 : 128, N, 0, 0);
+    const uint32_t base = smem_addr(smem);
+    for (int it = 0; it < iters; ++it) {
+      const int cs = it & 3;
+      const uint32_t la = base + cs * stage_bytes, ca = la + a_bytes;
+#pragma unroll
+      for (int kk = 0; kk < 4; ++kk) {
+        const uint64_t ad = umma_desc_sw128(la + kk * 32, 16, 1024), bd = umma_desc_sw128(ca + kk * 32, 16, 1024);
+        const uint32_t acc = (it | kk) != 0;
+        asm volatile(
+            "{\n.reg .pred p, q;\n"
+            "elect.sync _|p, 0xffffffff;\n"
+            "setp.ne.b32 q, %4, 0;\n"
+            "@p tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, q;\n}\n" ::"r"(tm),
+            "l"(ad), "l"(bd), "r"(idesc), "r"(acc)
+            : "memory");
+      }
+    }
+    asm volatile("{\n.reg .pred p;\nelect.sync _|p, 0xffffffff;\n@p tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n}\n" ::"r"(smem_addr(done)) : "memory");
   } else if (warp == 1 && lane == 0 && rank == 0) {
     int cs = 0, ph = 0;
     const uint32_t amn = (mma_on >= 5) ? 1u : 0u, bmn = (mma_on == 6) ? 1u : 0u;
@@ -109,6 +130,7 @@ int main() {
   unsigned long long* out; cudaMalloc(&out, 148 * 8);
   const int ctas = 148, iters = 4000;
   struct Cfg { int pair, N, S, mma, big = 0; } cfgs[] = {
+      {0, 256, 4, 2}, {0, 256, 4, 7}, {0, 128, 4, 2}, {0, 128, 4, 7}, {0, 64, 4, 2}, {0, 64, 4, 7}, {0, 32, 4, 7},
       {0, 64, 8, 1, 1}, {0, 64, 8, 1, 0}, {0, 256, 4, 1, 1},
       {0, 64, 4, 5}, {0, 128, 4, 5}, {0, 256, 4, 5}, {0, 64, 4, 6}, {0, 128, 4, 6}, {1, 128, 4, 5}, {1, 64, 4, 5},
       {0, 128, 4, 2}, {0, 128, 4, 3}, {0, 128, 4, 4}, {0, 64, 4, 2}, {0, 64, 4, 3}, {0, 64, 4, 4}, {0, 32, 4, 4}, {1, 128, 4, 3}, {1, 64, 4, 4},

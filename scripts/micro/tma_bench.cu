@@ -15,7 +15,7 @@ struct Maps { CUtensorMap a; CUtensorMap b; };
 
 template <int MODE, int MASK = 0>  // 0 single-CTA, 1 cluster-2 with cta_group::2 TMA, 2 cluster-2 plain TMA
 __global__ void __launch_bounds__(192, 1) tma_kernel(const __grid_constant__ Maps maps_p, int iters, int S,
-                                                    int a_rows, int b_rows, unsigned long long* out, const Maps* gmaps, int ndesc) {
+                                                    int a_rows, int b_rows, unsigned long long* out, const Maps* gmaps, int ndesc, int big, int R_rows) {
   const Maps& maps0 = gmaps ? *gmaps : maps_p;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -25,7 +25,7 @@ __global__ void __launch_bounds__(192, 1) tma_kernel(const __grid_constant__ Map
   uint32_t rank = 0;
   if (MODE != 0) rank = cluster_ctarank();
   if (threadIdx.x == 0) {
-    for (int s = 0; s < S; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], MODE == 1 ? 1 : 1); }
+    for (int s = 0; s < S; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], MODE == 4 ? 2 : 1); }
     mbar_init(&empty[15], 1);
     fence_barrier_init();
   }
@@ -39,8 +39,19 @@ __global__ void __launch_bounds__(192, 1) tma_kernel(const __grid_constant__ Map
       uint8_t* dst = smem + ps * stage_bytes;
       int k0 = (it % 64) * 64;
       const Maps& maps = (gmaps && ndesc > 1) ? gmaps[(it + blockIdx.x) % ndesc] : maps0;
-      int row = ((blockIdx.x * 7 + it / 64) % 16) * 256;
-      if (MODE == 1) {
+      int row = big ? ((blockIdx.x * 64 + it / 64) * 256) % (R_rows - 512) : ((blockIdx.x * 7 + it / 64) % 16) * 256;
+      if (MODE == 4) {
+        // own lane box (a_rows) + half of a 2*b_rows col tile, multicast to both CTAs
+        mbar_arrive_expect_tx(&full[ps], (a_rows + 2 * b_rows) * 128);
+        tma_load_3d(dst, &maps.a, &full[ps], k0, row, 0);
+        const uint32_t half_dst = smem_addr(dst + a_rows * 128 + rank * b_rows * 128);
+        asm volatile(
+            "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes.multicast::cluster"
+            " [%0], [%1, {%3, %4, %5}], [%2], %6;" ::"r"(half_dst),
+            "l"(reinterpret_cast<uint64_t>(&maps.b)), "r"(smem_addr(&full[ps])), "r"(k0), "r"(row + 128 + (int)rank * b_rows), "r"(0),
+            "h"((uint16_t)0x3)
+            : "memory");
+      } else if (MODE == 1) {
         uint32_t fb = MASK ? (smem_addr(&full[ps]) & 0xFEFFFFFFu) : mapa_shared(smem_addr(&full[ps]), 0);
         if (rank == 0) mbar_arrive_expect_tx(&full[ps], 2 * stage_bytes);
         tma_load_3d_pair(dst, &maps.a, fb, k0, row, 0);
@@ -56,7 +67,11 @@ __global__ void __launch_bounds__(192, 1) tma_kernel(const __grid_constant__ Map
     int cs = 0, ph = 0;
     for (int it = 0; it < iters; ++it) {
       mbar_wait(&full[cs], ph);
-      if (MODE == 1) {
+      if (MODE == 4) {
+        // both CTAs must have consumed stage cs before either re-fills it (multicast writes both)
+        asm volatile("mbarrier.arrive.relaxed.cluster.shared::cluster.b64 _, [%0];" ::"r"(mapa_shared(smem_addr(&empty[cs]), 0)) : "memory");
+        asm volatile("mbarrier.arrive.relaxed.cluster.shared::cluster.b64 _, [%0];" ::"r"(mapa_shared(smem_addr(&empty[cs]), 1)) : "memory");
+      } else if (MODE == 1) {
         asm volatile("mbarrier.arrive.relaxed.cluster.shared::cluster.b64 _, [%0];" ::"r"(mapa_shared(smem_addr(&empty[cs]), 0)) : "memory");
         asm volatile("mbarrier.arrive.relaxed.cluster.shared::cluster.b64 _, [%0];" ::"r"(mapa_shared(smem_addr(&empty[cs]), 1)) : "memory");
       } else {
@@ -88,13 +103,13 @@ static void make(CUtensorMap* m, void* base, int64_t inner, int64_t rows, uint32
 }
 
 int main() {
-  const int64_t K = 4096, R = 4096;
+  const int64_t K = 4096, R = 65536;  // 512 MiB: BIG mode streams from HBM
   void* buf; cudaMalloc(&buf, K * R * 2); cudaMemset(buf, 0, K * R * 2);
   unsigned long long* out; cudaMalloc(&out, 148 * 8);
   int ctas = 148, iters = 2000;
   Maps* dmaps; cudaMalloc(&dmaps, 512 * sizeof(Maps));
-  struct Cfg { int mode, a, b, S; const char* name; int gm = 0; int spin = 0; } cfgs[] = {
-      {0, 128, 128, 6, "GMEM-desc single 128+128 S6", 1}, {0, 128, 128, 6, "GMEM 8 descs", 8}, {0, 128, 128, 6, "GMEM 64 descs", 64}, {0, 128, 128, 6, "GMEM 512 descs", 512}, {0, 128, 128, 6, "single + 4 spinning warps", 0, 1}, {0, 128, 256, 4, "single 128+256 + 4 spinning warps", 0, 1}, {1, 128, 128, 6, "GMEM-desc pair 128+128 S6", 1},
+  struct Cfg { int mode, a, b, S; const char* name; int gm = 0; int spin = 0; int big = 0; } cfgs[] = {
+      {0, 128, 256, 4, "BIG single 128+256 S4", 0, 0, 1}, {1, 128, 128, 6, "BIG pair 128+128 S6", 0, 0, 1}, {2, 128, 128, 6, "BIG cluster2 plain 128+128 S6", 0, 0, 1}, {0, 128, 128, 6, "BIG single 128+128 S6", 0, 0, 1}, {0, 128, 256, 4, "single 128+256 S4 (same ingest)", 0}, {0, 128, 128, 6, "GMEM-desc single 128+128 S6", 1}, {0, 128, 128, 6, "GMEM 8 descs", 8}, {0, 128, 128, 6, "GMEM 64 descs", 64}, {0, 128, 128, 6, "GMEM 512 descs", 512}, {0, 128, 128, 6, "single + 4 spinning warps", 0, 1}, {0, 128, 256, 4, "single 128+256 + 4 spinning warps", 0, 1}, {1, 128, 128, 6, "GMEM-desc pair 128+128 S6", 1},
       {0, 128, 256, 4, "single 128+256 S4"}, {0, 128, 128, 6, "single 128+128 S6"}, {0, 128, 64, 8, "single 128+64 S8"},
       {0, 128, 0, 8, "single 128 only S8"}, {0, 256, 0, 6, "single 256 only S6"},
       {1, 128, 128, 6, "pair(cta_group::2) 128+128 S6"}, {1, 128, 64, 8, "pair 128+64 S8"}, {3, 128, 128, 6, "pair masked-bar 128+128 S6"},
@@ -105,7 +120,7 @@ int main() {
     make(&m.a, buf, K, R, c.a > 0 ? (c.a > 256 ? 256 : c.a) : 64);
     make(&m.b, buf, K, R, c.b > 0 ? c.b : 64);
     for (int d = 0; d < 512; ++d) cudaMemcpy(dmaps + d, &m, sizeof(Maps), cudaMemcpyHostToDevice);
-    int smem = c.S * (c.a + c.b) * 128 + 2048;
+    int smem = c.S * (c.a + (c.mode == 4 ? 2 : 1) * c.b) * 128 + 2048;
     cudaLaunchConfig_t lc = {};
     lc.gridDim = dim3(ctas); lc.blockDim = dim3(c.spin ? 192 : 64); lc.dynamicSmemBytes = smem;
     cudaLaunchAttribute at[1];
@@ -115,13 +130,15 @@ int main() {
     cudaError_t e;
     auto launch = [&](int it) {
       if (c.mode == 0) { cudaFuncSetAttribute(tma_kernel<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-        e = cudaLaunchKernelEx(&lc, tma_kernel<0>, m, it, c.S, c.a, c.b, out, c.gm ? dmaps : nullptr, c.gm); }
+        e = cudaLaunchKernelEx(&lc, tma_kernel<0>, m, it, c.S, c.a, c.b, out, c.gm ? dmaps : nullptr, c.gm, c.big, (int)R); }
       else if (c.mode == 3) { cudaFuncSetAttribute(tma_kernel<1, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-        e = cudaLaunchKernelEx(&lc, tma_kernel<1, 1>, m, it, c.S, c.a, c.b, out, c.gm ? dmaps : nullptr, c.gm); }
+        e = cudaLaunchKernelEx(&lc, tma_kernel<1, 1>, m, it, c.S, c.a, c.b, out, c.gm ? dmaps : nullptr, c.gm, c.big, (int)R); }
+      else if (c.mode == 4) { cudaFuncSetAttribute(tma_kernel<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+        e = cudaLaunchKernelEx(&lc, tma_kernel<4>, m, it, c.S, c.a, c.b, out, c.gm ? dmaps : nullptr, c.gm, c.big, (int)R); }
       else if (c.mode == 1) { cudaFuncSetAttribute(tma_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-        e = cudaLaunchKernelEx(&lc, tma_kernel<1>, m, it, c.S, c.a, c.b, out, c.gm ? dmaps : nullptr, c.gm); }
+        e = cudaLaunchKernelEx(&lc, tma_kernel<1>, m, it, c.S, c.a, c.b, out, c.gm ? dmaps : nullptr, c.gm, c.big, (int)R); }
       else { cudaFuncSetAttribute(tma_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-        e = cudaLaunchKernelEx(&lc, tma_kernel<2>, m, it, c.S, c.a, c.b, out, c.gm ? dmaps : nullptr, c.gm); }
+        e = cudaLaunchKernelEx(&lc, tma_kernel<2>, m, it, c.S, c.a, c.b, out, c.gm ? dmaps : nullptr, c.gm, c.big, (int)R); }
     };
     launch(100); cudaDeviceSynchronize();
     cudaEvent_t e0, e1; cudaEventCreate(&e0); cudaEventCreate(&e1);
