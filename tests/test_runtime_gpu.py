@@ -97,3 +97,26 @@ def test_e2e_pipelined_round_trip(cuda, planner):
     assert torch.allclose(host.float(), ss.out_arena.float(), rtol=0, atol=0, equal_nan=True)
     for i, x in enumerate(ss.bound):
         assert rel(x.C, ss.reference_outputs(i)) < 2e-2
+
+
+def test_c4_sweep_sample_one_table(cuda, planner):
+    """A sample of the C4 10k-shape sweep (mixed Dense / attention BMM, M and T
+    dynamic) planned and executed as ONE table. Size-independent check on every
+    shape: row checksums C @ 1 == A @ (B @ 1) in float64 (scaled by the row
+    sums of |C|); shapes small enough also get the full element-wise check."""
+    from paper_2407_21418_b200.workloads import c4_shapes
+
+    shapes = c4_shapes(48, seed=11)
+    ss = ShapeSet(shapes, planner, device=cuda, seed=11)
+    ss.out_arena.fill_(float("nan"))
+    ss.launch()
+    torch.cuda.synchronize()
+    for i, x in enumerate(ss.bound):
+        C = x.C.double()
+        assert not torch.isnan(C).any(), x.shape
+        Bkn = x.B.double().transpose(-1, -2) if x.shape.b_layout == "nk" else x.B.double()
+        expect = (x.A.double() @ Bkn.sum(-1, keepdim=True)).squeeze(-1)
+        err = (C.sum(-1) - expect).abs().max() / C.abs().sum(-1).max().clamp_min(1e-30)
+        assert err.item() < 1e-2, x.shape
+        if x.shape.flops < 2e9:
+            assert rel(x.C, ss.reference_outputs(i)) < 2e-2, x.shape
