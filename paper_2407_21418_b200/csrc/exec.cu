@@ -202,6 +202,8 @@ struct ExecImpl {
   std::vector<int32_t> pack_rows;     // per problem: lane box rows when packed
   TcWork* d_tcwork = nullptr;
   TcPair* d_tcpairs = nullptr;
+  float* d_split_ws = nullptr;        // split-K fp32 partials
+  int32_t* d_split_cnt = nullptr;     // split-K arrival counters (self-resetting)
   unsigned long long* d_trace = nullptr;
   TcConfig cfg{};    // single-CTA kernel (K1)
   TcConfig cfg2{};   // CTA-pair kernel (K1b)
@@ -213,6 +215,8 @@ struct ExecImpl {
     if (d_maps) cudaFree(d_maps);
     if (d_tcwork) cudaFree(d_tcwork);
     if (d_tcpairs) cudaFree(d_tcpairs);
+    if (d_split_ws) cudaFree(d_split_ws);
+    if (d_split_cnt) cudaFree(d_split_cnt);
     if (d_trace) cudaFree(d_trace);
   }
 };
@@ -520,6 +524,52 @@ static void upload(ExecImpl& I) {
     max_n = std::max(max_n, w.n_mma);
     tw.push_back(t);
   }
+  // Split-K: a table too small to occupy the SMs (e.g. one skinny Dense, or a
+  // mid-size shape timed alone) splits each plain item's K blocks over up to
+  // kMaxSplit items; partials meet in an fp32 workspace and the last warp to
+  // arrive per lane quadrant reduces and stores (kernel_tc.cu). Tables that
+  // already fill the GPU (the grouped C1 step) are left alone.
+  {
+    int sms_here = device_sms();
+    if (sms_here <= 0) sms_here = 148;
+    const char* env_sk = std::getenv("FTB_SPLITK");
+    const bool split_on = !(env_sk && env_sk[0] == '0') && !pairing;
+    const int64_t n_items = static_cast<int64_t>(tw.size());
+    if (split_on && n_items > 0 && n_items * 2 <= sms_here) {
+      const int target = static_cast<int>(std::min<int64_t>(kMaxSplit, sms_here / n_items));
+      std::vector<TcWork> split;
+      int32_t tiles = 0;
+      for (const TcWork& t : tw) {
+        // >= 8 K blocks per split, and only narrow tiles: the fp32 partial
+        // round trip (128 x n_mma x 8 B) must stay small next to the operand
+        // bytes a split saves (measured: C3 M<=127 22 -> 18 us, M=256 n=256
+        // tiles 23 -> 28 us when split)
+        const int s_t = t.n_mma <= 128 ? std::min(target, t.num_kb / 8) : 1;
+        if (t.pack || s_t < 2) {
+          split.push_back(t);
+          continue;
+        }
+        const int32_t tile = tiles++;
+        for (int q = 0; q < s_t; ++q) {
+          TcWork u = t;
+          const int kb0 = static_cast<int>(static_cast<int64_t>(t.num_kb) * q / s_t);
+          const int kb1 = static_cast<int>(static_cast<int64_t>(t.num_kb) * (q + 1) / s_t);
+          u.num_kb = kb1 - kb0;
+          u.flags |= kFlagSplitK;
+          u.pack = static_cast<uint32_t>(kb0) | (static_cast<uint32_t>(s_t) << 16) |
+                   (static_cast<uint32_t>(q) << 24);
+          u.c_bs = tile;
+          split.push_back(u);
+        }
+      }
+      if (tiles > 0) {
+        FTB_CUDA(cudaMalloc(&I.d_split_ws, sizeof(float) * static_cast<size_t>(tiles) * kSplitTileFloats));
+        FTB_CUDA(cudaMalloc(&I.d_split_cnt, sizeof(int32_t) * 4 * tiles));
+        FTB_CUDA(cudaMemset(I.d_split_cnt, 0, sizeof(int32_t) * 4 * tiles));
+        tw.swap(split);
+      }
+    }
+  }
   I.n_singles = static_cast<int64_t>(tw.size());
   I.n_pairs = static_cast<int64_t>(pairs.size());
   if (!tw.empty()) {
@@ -552,6 +602,8 @@ static void upload(ExecImpl& I) {
     c.trace = nullptr;
   };
   shape_cfg(I.cfg, max_n, max_n);
+  I.cfg.split_ws = I.d_split_ws;
+  I.cfg.split_cnt = I.d_split_cnt;
   int max_np = 32;
   for (const TcPair& t : pairs) max_np = std::max(max_np, t.n_mma);
   shape_cfg(I.cfg2, max_np, max_np / 2);

@@ -64,7 +64,13 @@ struct alignas(16) DevWork {
 //   kFlagTmaStore: the item's rectangle is whole 32 x 32 store boxes or ends
 //   at the tensor edge, so the epilogue may store through TMA (clipped by the
 //   hardware) instead of predicated st.global.
-enum : uint32_t { kFlagSwap = 1u, kFlagLaneMN = 2u, kFlagColMN = 4u, kFlagOutF32 = 8u, kFlagTmaStore = 16u };
+//   kFlagSplitK: the item computes K blocks [kb0, kb0 + num_kb) of a tile split
+//   over nsplit items (pack = kb0 | nsplit << 16 | split << 24, c_bs = tile);
+//   partials meet in the fp32 workspace and the last warp per lane quadrant
+//   to arrive sums them and stores C (exec.cu, kernel_tc.cu).
+enum : uint32_t {
+  kFlagSwap = 1u, kFlagLaneMN = 2u, kFlagColMN = 4u, kFlagOutF32 = 8u, kFlagTmaStore = 16u, kFlagSplitK = 32u
+};
 // Block-diagonal batch packing (short attention BMMs, exec.cu): `pack` holds
 // nb (entries in this item, bits 0-7), the TMA box depth (bits 8-15) and the
 // lane slot rows (32 or 64, bits 16-31); entry e of the item is batch
@@ -86,6 +92,12 @@ __host__ __device__ inline int pack_nb(uint32_t p) { return p ? static_cast<int>
 __host__ __device__ inline int pack_depth(uint32_t p) { return static_cast<int>((p >> 8) & 0xFFu); }
 __host__ __device__ inline int pack_lane_rows(uint32_t p) { return static_cast<int>(p >> 16); }
 constexpr int kMaxPack = 4;
+__host__ __device__ inline int split_kb0(uint32_t p) { return static_cast<int>(p & 0xFFFFu); }
+__host__ __device__ inline int split_n(uint32_t p) { return static_cast<int>((p >> 16) & 0xFFu); }
+__host__ __device__ inline int split_idx(uint32_t p) { return static_cast<int>(p >> 24); }
+constexpr int kMaxSplit = 8;
+constexpr int kSplitRowFloats = 256;                          // columns per tile in the workspace
+constexpr int kSplitTileFloats = kMaxSplit * 128 * kSplitRowFloats;
 
 // CTA-pair work item (64 B): two 128-lane slabs (one per CTA of a cluster
 // pair) that share the column operand; N = n_mma columns, each CTA stages
@@ -109,6 +121,8 @@ struct TcConfig {
   int32_t n_acc;           // TMEM accumulator slots (2, 4 or 8)
   int32_t acc_cols;        // columns per slot (512 / n_acc)
   unsigned long long* trace;  // optional: per-CTA phase timestamps (debug)
+  float* split_ws;            // split-K partials [tile][split][128][256] fp32
+  int32_t* split_cnt;         // split-K arrivals [tile][4 lane quadrants]
 };
 constexpr int kTraceItems = 16;   // items traced per CTA
 constexpr int kTraceEvents = 6;   // see kernel_tc.cu

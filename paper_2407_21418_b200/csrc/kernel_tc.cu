@@ -70,6 +70,63 @@ __device__ __forceinline__ TcWork bcast_work(uint32_t mine) {
   return it;
 }
 
+// Split-K epilogue for one warp (lane quadrant): publish the fp32 partial of
+// this split to the workspace, count the arrival; the last of the tile's
+// splits for this quadrant sums all partials (fixed split order, so the sum is
+// deterministic) and stores C through the predicated path, then re-arms the
+// counter for the next launch.
+template <class Release>
+__device__ __forceinline__ void split_epilogue(const TcConfig& cfg, const TcWork& it, uint8_t* region, uint32_t taddr,
+                                               int lane_base, bool swap, bool f32, Release release) {
+  const int lane = threadIdx.x & 31;
+  const int quad = lane_base >> 5;
+  const int nsplit = split_n(it.pack), me = split_idx(it.pack), tile = it.c_bs;
+  // workspace: [tile][split][quad][chunk][32 cols][32 lanes] — every access is
+  // one coalesced 128-B row per register index
+  float* ws = cfg.split_ws + static_cast<size_t>(tile) * kSplitTileFloats;
+  auto part = [&](int split, int c0) {
+    return ws + ((static_cast<size_t>(split) * 4 + quad) * (kSplitRowFloats / 32) + (c0 >> 5)) * 1024 + lane;
+  };
+  for (int c0 = 0; c0 < it.col_len; c0 += 32) {
+    uint32_t raw[32];
+    tmem_ld_32x32b_x32(taddr + c0, raw);
+    tmem_ld_wait();
+    float* dst = part(me, c0);
+#pragma unroll
+    for (int e = 0; e < 32; ++e) dst[e * 32] = __uint_as_float(raw[e]);
+  }
+  release();  // TMEM no longer needed
+  __threadfence();
+  __syncwarp();
+  int32_t* cnt = cfg.split_cnt + tile * 4 + quad;
+  int arrived = 0;
+  if (lane == 0) arrived = atomicAdd(cnt, 1);
+  arrived = __shfl_sync(0xffffffffu, arrived, 0);
+  if (arrived != nsplit - 1) return;  // not the last split of this quadrant
+  __threadfence();
+  if (lane == 0) *cnt = 0;  // re-arm for the next launch (stream order separates launches)
+  if (lane_base >= it.lane_len) return;
+  float* tb = reinterpret_cast<float*>(region);
+  if (lane == 0) bulk_wait_read<0>();  // the transpose tile aliases this warp's store boxes
+  __syncwarp();
+  for (int c0 = 0; c0 < it.col_len; c0 += 32) {
+    float v[32];
+#pragma unroll
+    for (int e = 0; e < 32; ++e) v[e] = 0.f;
+    for (int sp = 0; sp < nsplit; ++sp) {  // fixed order: deterministic sum
+      const float* src = part(sp, c0);
+#pragma unroll
+      for (int e = 0; e < 32; ++e) v[e] += __ldcg(src + e * 32);
+    }
+    const int ncol = min(32, it.col_len - c0);
+    const int nlane = min(32, it.lane_len - lane_base);
+    if (!swap)
+      store_block32(tb, v, true, it.C, it.ldc, it.lane0 + lane_base, it.col0 + c0, nlane, ncol, f32);
+    else
+      store_block32(tb, v, false, it.C, it.ldc, it.col0 + c0, it.lane0 + lane_base, ncol, nlane, f32);
+  }
+}
+
 template <int S>
 __global__ void __launch_bounds__(kTcThreads, 1)
     ftb_tc_kernel(const TcWork* __restrict__ work, int32_t n_work, TcConfig cfg) {
@@ -144,7 +201,9 @@ __global__ void __launch_bounds__(kTcThreads, 1)
       }
       const CUtensorMap* tl = &it.maps->lane;
       const bool lane_mn = it.flags & kFlagLaneMN, col_mn = it.flags & kFlagColMN;
-      const int depth = pack_depth(it.pack);  // 0: not packed
+      const bool splitk = it.flags & kFlagSplitK;
+      const int kb_base = splitk ? split_kb0(it.pack) : 0;
+      const int depth = splitk ? 0 : pack_depth(it.pack);  // 0: not packed
       const uint32_t bytes =
           depth ? static_cast<uint32_t>(depth * (pack_lane_rows(it.pack) + 64) * kBlockK * 2)
                 : kLaneStageBytes + static_cast<uint32_t>(it.n_mma) * kBlockK * 2;
@@ -178,7 +237,7 @@ __global__ void __launch_bounds__(kTcThreads, 1)
           mbar_arrive_expect_tx(&full[s], bytes);
           uint8_t* ldst = lane_buf + s * kLaneStageBytes;
           uint8_t* cdst = col_buf + s * cfg.col_stage_bytes;
-          const int k0 = kb * kBlockK;
+          const int k0 = (kb + kb_base) * kBlockK;
           if (depth) {  // packed batch entries: one 3-D box per operand
             tma_load_3d(ldst, tl, &full[s], k0, it.lane0, it.batch);
             if (!col_mn) tma_load_3d(cdst, &it.maps->col[0], &full[s], k0, it.col0, it.batch);
@@ -330,7 +389,9 @@ __global__ void __launch_bounds__(kTcThreads, 1)
         __syncwarp();
         if (lane == 0) mbar_arrive(&tempty[slot]);
       };
-      if (!it.pack) {
+      if (it.flags & kFlagSplitK) {
+        split_epilogue(cfg, it, region, taddr, lane_base, swap, f32, release);
+      } else if (!it.pack) {
         epilogue_tile(region, ngrp, taddr, lane_base < it.lane_len, tma, swap, f32, &it.maps->out, it.C, it.ldc,
                       it.lane0, it.lane_len, lane_base, it.col0, it.col_len, it.batch, release);
       } else {

@@ -55,14 +55,17 @@ def test_dense_bf16(cuda, case, b_layout, orientation):
 
 @pytest.mark.parametrize("case", DENSE_CASES, ids=lambda c: f"M{c[0]}N{c[1]}K{c[2]}")
 @pytest.mark.parametrize("b_layout", ["kn", "nk"])
-@pytest.mark.parametrize("mode", ["pair", "no_tma_store"])
+@pytest.mark.parametrize("mode", ["pair", "no_tma_store", "no_splitk"])
 def test_dense_bf16_kernel_modes(cuda, case, b_layout, mode, monkeypatch):
-    """The CTA-pair kernel (FTB_PAIR=1) and the predicated st.global epilogue
-    (FTB_TMA_STORE=0) against the same reference as the default path."""
+    """The CTA-pair kernel (FTB_PAIR=1), the predicated st.global epilogue
+    (FTB_TMA_STORE=0) and the unsplit K loop (FTB_SPLITK=0; small tables split
+    K by default) against the same reference as the default path."""
     if mode == "pair":
         monkeypatch.setenv("FTB_PAIR", "1")
-    else:
+    elif mode == "no_tma_store":
         monkeypatch.setenv("FTB_TMA_STORE", "0")
+    else:
+        monkeypatch.setenv("FTB_SPLITK", "0")
     M, N, K, tau, parts = case
     A, B, ref = _dense(M, N, K, b_layout, torch.bfloat16, cuda, seed=5)
     Cout = torch.full((M, N), float("nan"), dtype=torch.bfloat16, device=cuda)
@@ -167,3 +170,21 @@ def test_dense_ffma_fp32(cuda, M, b_layout):
     torch.cuda.synchronize()
     assert ex.info.kernel == "ffma"
     assert _rel(Cout, ref) < F32_TOL
+
+
+def test_split_k_repeated_launches_deterministic(cuda):
+    """Split-K counters re-arm themselves: repeated launches (and a CUDA graph
+    replay) give bit-identical results (fixed summation order)."""
+    M, N, K = 64, 1024, 4096
+    A, B, ref = _dense(M, N, K, "nk", torch.bfloat16, cuda, seed=21)
+    Cout = torch.empty(M, N, dtype=torch.bfloat16, device=cuda)
+    ex = Executable([gemm_desc(A, B, Cout, "nk")], [program_struct(2, 1, [((1, 1), (64, 256, 64), 4)])])
+    ex.launch()
+    torch.cuda.synchronize()
+    first = Cout.clone()
+    assert _rel(Cout, ref) < BF16_TOL
+    for _ in range(3):
+        Cout.zero_()
+        ex.launch()
+    torch.cuda.synchronize()
+    assert torch.equal(Cout, first)
