@@ -210,17 +210,21 @@ ftb_status ftb_plan_batch(const ftb_hw* hw, const ftb_instance* insts, int32_t n
           // Parity mode ranks the final set only (an empty pool raises, as
           // combine.py:183-188 does). B200 mode walks a documented fallback
           // ladder when no combination covers tau: ranked set final -> filter
-          // -> cross -> align; then the same with the main-axis tile relaxed,
-          // first to any wide MMA N (multiple of 32 in [128, 256]), then to any
-          // size <= 256 (padded inside the MMA tile); then parity mode.
-          // Reported stage = set index + 4 * rung.
-          struct Rung { int legality, relax, level; };
+          // -> cross -> align; for a Dense, then the same with the other output
+          // axis as the composition axis (its extent may be a multiple of the
+          // strict 256-column tile when the main axis is not); then with the
+          // main-axis tile relaxed, first to any wide MMA N (multiple of 32 in
+          // [128, 256]), then to any size <= 256 (padded inside the MMA tile);
+          // then parity mode. Reported stage = set index + 4 * rung.
+          struct Rung { int legality, relax, level, tau; };
           std::vector<Rung> rungs;
           if (h.legality) {
             const int tau = select_main_axis(in);
-            rungs = {{1, -1, 0}, {1, tau, 1}, {1, tau, 2}, {0, -1, 0}};
+            rungs = {{1, -1, 0, -1}};
+            if (in.ns == 2) rungs.push_back({1, -1, 0, 1 - tau});
+            rungs.insert(rungs.end(), {{1, tau, 1, -1}, {1, tau, 2, -1}, {0, -1, 0, -1}});
           } else {
-            rungs = {{0, -1, 0}};
+            rungs = {{0, -1, 0, -1}};
           }
           bool done = false;
           for (size_t ri = 0; ri < rungs.size() && !done; ++ri) {
@@ -232,6 +236,7 @@ ftb_status ftb_plan_batch(const ftb_hw* hw, const ftb_instance* insts, int32_t n
             for (int stage = 0; stage <= last && !done; ++stage) {
               try {
                 Cands c = compile_shape(in, hq, q, &r, stage);
+                if (rungs[ri].tau >= 0) r.tau = rungs[ri].tau;
                 auto top = rank_topk(c, r.tau, *coeffs, 1, false);
                 if (top.empty()) throw FtbError(FTB_EMPTY_RESULT, "empty program pool", "program pool");
                 fill_program(c, r.tau, top[0].first, top[0].second, &out[i]);
