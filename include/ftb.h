@@ -173,6 +173,8 @@ enum { FTB_OP_DENSE = 0, FTB_OP_BMM = 1 };
 enum { FTB_B_KN = 0, /* B stored [K,N], N contiguous (MN-major operand)  */
        FTB_B_NK = 1  /* B stored [N,K], K contiguous (K-major, nn.Linear) */ };
 enum { FTB_DT_BF16 = 0, FTB_DT_F32 = 1 };
+/* Fused epilogue (Dense only): C = act(A·B + bias), bias[N] in bias_dtype. */
+enum { FTB_ACT_NONE = 0, FTB_ACT_GELU = 1 /* erf form, as torch.nn.functional.gelu */ };
 
 /* One GEMM problem bound to device buffers. Strides are in elements.
  * Batch strides are ignored for dense (batch = 1). The tcgen05 path needs
@@ -188,6 +190,9 @@ typedef struct {
   int32_t in_dtype;      /* FTB_DT_BF16 (tcgen05) / FTB_DT_F32 (FFMA mode) */
   int32_t out_dtype;     /* FTB_DT_BF16 / FTB_DT_F32                       */
   int32_t orientation;   /* -1 auto, 0 lanes=i (normal), 1 lanes=j (swap-AB) */
+  const void* bias;      /* NULL or bias[N] added per output column (Dense) */
+  int32_t bias_dtype;    /* FTB_DT_BF16 / FTB_DT_F32                       */
+  int32_t activation;    /* FTB_ACT_NONE / FTB_ACT_GELU                    */
 } ftb_gemm_desc;
 
 typedef struct ftb_exec ftb_exec;   /* lowered tile-schedule table on device */

@@ -28,6 +28,7 @@ FTB_CUDA_ERROR = 6
 OP_DENSE, OP_BMM = 0, 1
 B_KN, B_NK = 0, 1
 DT_BF16, DT_F32 = 0, 1
+ACT_NONE, ACT_GELU = 0, 1
 
 
 class Program(C.Structure):
@@ -63,6 +64,9 @@ class GemmDesc(C.Structure):
         ("in_dtype", C.c_int32),
         ("out_dtype", C.c_int32),
         ("orientation", C.c_int32),
+        ("bias", C.c_void_p),
+        ("bias_dtype", C.c_int32),
+        ("activation", C.c_int32),
     ]
 
 

@@ -6,6 +6,7 @@
 #include <cuda_bf16.h>
 #include <cstdint>
 
+#include "exec_types.h"
 #include "ptx.cuh"
 
 namespace ftb {
@@ -161,6 +162,27 @@ __device__ __forceinline__ void stage_box_bf16(uint8_t* box, const uint32_t (&r)
   }
 }
 
+// ---------------------------------------------------------------- fused epilogue op
+__device__ __forceinline__ float gelu_erf(float x) { return 0.5f * x * (1.f + erff(x * 0.70710678118654752f)); }
+__device__ __forceinline__ float load_bias(const EpiOp& op, int c) {
+  if (!op.bias || c < 0 || c >= op.n) return 0.f;
+  return op.bias_f32 ? __ldg(static_cast<const float*>(op.bias) + c)
+                     : __bfloat162float(static_cast<const __nv_bfloat16*>(op.bias)[c]);
+}
+// acc + bias[column], then the activation, on a warp's 32 x 32 chunk (fp32 bits
+// in `r`). lane_is_row: lane l is a C row and register e is C column
+// col_base + e; otherwise lane l is C column col_base + l (every register).
+__device__ __forceinline__ void apply_epi(uint32_t (&r)[32], const EpiOp& op, bool lane_is_row, int col_base) {
+  const int l = threadIdx.x & 31;
+  const float bl = load_bias(op, col_base + l);
+#pragma unroll
+  for (int e = 0; e < 32; ++e) {
+    float x = __uint_as_float(r[e]) + (lane_is_row ? __shfl_sync(0xffffffffu, bl, e) : bl);
+    if (op.act == 1) x = gelu_erf(x);
+    r[e] = __float_as_uint(x);
+  }
+}
+
 // One epilogue warp's share of a finished work item: TMEM lanes
 // [lane_base, lane_base + 32) of the accumulator at `taddr`, columns
 // [0, col_len). C-side coordinates: normal orientation (swap = false) stores
@@ -168,11 +190,12 @@ __device__ __forceinline__ void stage_box_bf16(uint8_t* box, const uint32_t (&r)
 // `release()` hands the accumulator back to the MMA warp right after the
 // last TMEM read. `region` is the warp's 8 KiB staging area (four 2 KiB TMA
 // boxes or the 32x33 fp32 transpose tile), `ngrp` its running box-group count.
+// `op` (or null): fused bias + activation applied before rounding.
 template <class Release>
 __device__ __forceinline__ void epilogue_tile(uint8_t* region, uint32_t& ngrp, uint32_t taddr, bool active, bool tma,
                                               bool swap, bool f32, const CUtensorMap* out_map, void* C, int64_t ldc,
                                               int lane0, int lane_len, int lane_base, int col0, int col_len, int batch,
-                                              Release release) {
+                                              Release release, const EpiOp* op = nullptr) {
   const int lane = threadIdx.x & 31;
   bool released = false;
   if (active) {
@@ -188,6 +211,10 @@ __device__ __forceinline__ void epilogue_tile(uint8_t* region, uint32_t& ngrp, u
         if (c0 + 64 >= col_len) {  // last TMEM read of the item
           release();
           released = true;
+        }
+        if (op) {  // normal: TMEM columns are C columns; swap-AB: lanes are
+          apply_epi(ra, *op, !swap, swap ? lane0 + lane_base : col0 + c0);
+          if (two) apply_epi(rb, *op, !swap, swap ? lane0 + lane_base : col0 + c0 + 32);
         }
         uint8_t* box = region + (ngrp & 1) * 4096;
         if (lane == 0) bulk_wait_read<1>();  // the group that last used these boxes has read them
@@ -217,6 +244,7 @@ __device__ __forceinline__ void epilogue_tile(uint8_t* region, uint32_t& ngrp, u
         uint32_t raw[32];
         tmem_ld_32x32b_x32(taddr + c0, raw);
         tmem_ld_wait();
+        if (op) apply_epi(raw, *op, !swap, swap ? lane0 + lane_base : col0 + c0);
         float v[32];
 #pragma unroll
         for (int e = 0; e < 32; ++e) v[e] = __uint_as_float(raw[e]);

@@ -260,6 +260,15 @@ static void build(ExecImpl& ex, const ftb_gemm_desc* probs, const ftb_program* p
     P.K = static_cast<int32_t>(d.K); P.batch = d.batch;
     P.out_f32 = d.out_dtype == FTB_DT_F32;
     P.b_nk = d.b_layout == FTB_B_NK;
+    if (d.activation != FTB_ACT_NONE && d.activation != FTB_ACT_GELU)
+      throw input_error("unknown activation", "activation");
+    if ((d.bias || d.activation != FTB_ACT_NONE) && d.op != FTB_OP_DENSE)
+      throw input_error("fused bias / activation epilogues are for Dense problems", "bias");
+    if (d.bias && d.bias_dtype != FTB_DT_BF16 && d.bias_dtype != FTB_DT_F32)
+      throw input_error("unsupported bias dtype", "bias_dtype");
+    P.bias = d.bias;
+    P.bias_f32 = d.bias_dtype == FTB_DT_F32;
+    P.act = d.activation;
     P.num_kb = static_cast<int32_t>(ceil_div(d.K, kBlockK));
     if (ffma && !P.out_f32) throw input_error("FFMA mode writes fp32 outputs", "out_dtype");
 
@@ -342,6 +351,11 @@ static void build(ExecImpl& ex, const ftb_gemm_desc* probs, const ftb_program* p
         }
       }
       ex.tma_out.push_back(encode_out_map(&m.out, d) ? 1 : 0);
+      m.epi.bias = d.bias;
+      m.epi.bias_f32 = d.bias_dtype == FTB_DT_F32;
+      m.epi.act = d.activation;
+      m.epi.n = static_cast<int32_t>(d.N);
+      m.epi.pad_ = 0;
       ex.maps.push_back(m);
     }
     ex.problems.push_back(P);
@@ -410,7 +424,7 @@ static void upload(ExecImpl& I) {
   FTB_CUDA(cudaMemcpy(I.d_maps, I.maps.data(), sizeof(DevMaps) * I.maps.size(), cudaMemcpyHostToDevice));
   auto flags_of = [](const DevProblem& P) {
     return (P.swap ? kFlagSwap : 0u) | (P.lane_mn ? kFlagLaneMN : 0u) | (P.col_mn ? kFlagColMN : 0u) |
-           (P.out_f32 ? kFlagOutF32 : 0u);
+           (P.out_f32 ? kFlagOutF32 : 0u) | ((P.bias || P.act) ? kFlagEpiOp : 0u);
   };
   auto c_of = [](const DevProblem& P, int32_t batch) {
     const size_t esz = P.out_f32 ? 4 : 2;

@@ -24,6 +24,18 @@ struct DevProblem {
   int32_t out_f32;            // C dtype: 0 bf16, 1 fp32
   int32_t b_nk;               // B stored [N,K]
   int32_t num_kb;             // ceil(K / 64)
+  const void* bias;           // fused epilogue: bias[N] (or null)
+  int32_t bias_f32;           // bias dtype: 0 bf16, 1 fp32
+  int32_t act;                // FTB_ACT_*
+};
+
+// Fused epilogue of one problem (Dense): C = act(acc + bias[col]).
+struct EpiOp {
+  const void* bias;  // bias[N] or null
+  int32_t bias_f32;
+  int32_t act;       // 0 none, 1 GELU (erf)
+  int32_t n;         // valid columns of C (bias length)
+  int32_t pad_;
 };
 
 // TMA descriptors of one problem for the tcgen05 kernel (64-B aligned).
@@ -36,6 +48,7 @@ struct alignas(64) DevMaps {
   CUtensorMap lane;
   CUtensorMap col[5];
   CUtensorMap out;
+  EpiOp epi;
 };
 constexpr int kColMaps = 5;
 
@@ -69,7 +82,8 @@ struct alignas(16) DevWork {
 //   partials meet in the fp32 workspace and the last warp per lane quadrant
 //   to arrive sums them and stores C (exec.cu, kernel_tc.cu).
 enum : uint32_t {
-  kFlagSwap = 1u, kFlagLaneMN = 2u, kFlagColMN = 4u, kFlagOutF32 = 8u, kFlagTmaStore = 16u, kFlagSplitK = 32u
+  kFlagSwap = 1u, kFlagLaneMN = 2u, kFlagColMN = 4u, kFlagOutF32 = 8u, kFlagTmaStore = 16u, kFlagSplitK = 32u,
+  kFlagEpiOp = 64u  // fused bias / activation: maps->epi
 };
 // Block-diagonal batch packing (short attention BMMs, exec.cu): `pack` holds
 // nb (entries in this item, bits 0-7), the TMA box depth (bits 8-15) and the

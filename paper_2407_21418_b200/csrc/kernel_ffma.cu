@@ -6,6 +6,7 @@
 // in the table's aux field; at fp32 the accumulation order is plain
 // sequential-K FFMA, which is what the 1e-5 tolerance is set against).
 // Orientation is always lanes = i, columns = j.
+#include <cuda_bf16.h>
 #include <cuda_runtime.h>
 
 #include "exec_types.h"
@@ -75,7 +76,13 @@ __global__ void __launch_bounds__(kFfmaThreads)
 #pragma unroll
       for (int b = 0; b < 4; ++b) {
         const int c = tx * 4 + b;
-        if (c < nj) C[static_cast<int64_t>(i0 + r) * P.ldc + j0 + c] = acc[a][b];
+        if (c >= nj) continue;
+        float x = acc[a][b];
+        if (P.bias)
+          x += P.bias_f32 ? static_cast<const float*>(P.bias)[j0 + c]
+                          : __bfloat162float(static_cast<const __nv_bfloat16*>(P.bias)[j0 + c]);
+        if (P.act == 1) x = 0.5f * x * (1.f + erff(x * 0.70710678118654752f));
+        C[static_cast<int64_t>(i0 + r) * P.ldc + j0 + c] = x;
       }
     }
   }

@@ -118,6 +118,14 @@ __device__ __forceinline__ void split_epilogue(const TcConfig& cfg, const TcWork
 #pragma unroll
       for (int e = 0; e < 32; ++e) v[e] += __ldcg(src + e * 32);
     }
+    if (it.flags & kFlagEpiOp) {
+      uint32_t rb[32];
+#pragma unroll
+      for (int e = 0; e < 32; ++e) rb[e] = __float_as_uint(v[e]);
+      apply_epi(rb, it.maps->epi, !swap, swap ? it.lane0 + lane_base : it.col0 + c0);
+#pragma unroll
+      for (int e = 0; e < 32; ++e) v[e] = __uint_as_float(rb[e]);
+    }
     const int ncol = min(32, it.col_len - c0);
     const int nlane = min(32, it.lane_len - lane_base);
     if (!swap)
@@ -393,7 +401,8 @@ __global__ void __launch_bounds__(kTcThreads, 1)
         split_epilogue(cfg, it, region, taddr, lane_base, swap, f32, release);
       } else if (!it.pack) {
         epilogue_tile(region, ngrp, taddr, lane_base < it.lane_len, tma, swap, f32, &it.maps->out, it.C, it.ldc,
-                      it.lane0, it.lane_len, lane_base, it.col0, it.col_len, it.batch, release);
+                      it.lane0, it.lane_len, lane_base, it.col0, it.col_len, it.batch, release,
+                      (it.flags & kFlagEpiOp) ? &it.maps->epi : nullptr);
       } else {
         // block-diagonal pack: this warp's lane quadrant belongs to entry e
         const int wpe = pack_lane_rows(it.pack) / 32;  // warps per entry

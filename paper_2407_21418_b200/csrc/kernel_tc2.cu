@@ -253,12 +253,15 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kTcThreads, 1)
       if (quad == 0 && lane == 0) trace2_ev(cfg, local, 4);
       const int lane_base = quad * 32;
       const uint32_t taddr = tmem_base + (static_cast<uint32_t>(lane_base) << 16) + slot * cfg.acc_cols;
-      epilogue_tile(region, ngrp, taddr, lane_base < lane_len, tma, swap, f32, &it.maps->out, it.C, it.ldc, lane0,
-                    lane_len, lane_base, it.col0, it.col_len, it.batch, [&] {
-                      tc_fence_before();
-                      __syncwarp();
-                      if (lane == 0) mbar_arrive_remote(smem_addr(&tempty[slot]) & kPeerBitMask);
-                    });
+      epilogue_tile(
+          region, ngrp, taddr, lane_base < lane_len, tma, swap, f32, &it.maps->out, it.C, it.ldc, lane0, lane_len,
+          lane_base, it.col0, it.col_len, it.batch,
+          [&] {
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive_remote(smem_addr(&tempty[slot]) & kPeerBitMask);
+          },
+          (it.flags & kFlagEpiOp) ? &it.maps->epi : nullptr);
       if (quad == 0 && lane == 0) trace2_ev(cfg, local, 5);
     }
     if (lane == 0) bulk_wait_all();  // output stores complete before the CTA retires

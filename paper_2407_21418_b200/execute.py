@@ -78,12 +78,17 @@ def _dt(t) -> int:
     raise TypeError(f"unsupported dtype {t.dtype}; use bfloat16 (tcgen05) or float32 (FFMA)")
 
 
-def gemm_desc(A, B, Cout, b_layout: str = "kn", orientation: int = -1) -> GemmDesc:
-    """Describe ``Cout = A @ B`` for 2-D (Dense) or 3-D (BatchMatmul) tensors.
+def gemm_desc(A, B, Cout, b_layout: str = "kn", orientation: int = -1, bias=None,
+              activation: str | None = None) -> GemmDesc:
+    """Describe ``Cout = act(A @ B + bias)`` for 2-D (Dense) or 3-D
+    (BatchMatmul) tensors.
 
     ``b_layout="kn"``: B is [K, N] (or [b, K, N]) as in the reference's access
     B[k, j]; ``"nk"``: B is given as its [N, K] transpose (nn.Linear weight
     layout). Only the last dimension of each tensor must be contiguous.
+    ``bias`` ([N], bf16 or fp32) and ``activation`` (None or ``"gelu"``, the
+    erf form of ``torch.nn.functional.gelu``) are fused into the epilogue
+    (Dense only).
     """
     d = GemmDesc()
     if A.dim() == 2:
@@ -114,6 +119,14 @@ def gemm_desc(A, B, Cout, b_layout: str = "kn", orientation: int = -1) -> GemmDe
         raise TypeError("A and B must share a dtype")
     d.out_dtype = _dt(Cout)
     d.orientation = orientation
+    if bias is not None:
+        if bias.dim() != 1 or bias.shape[0] != d.N or not bias.is_cuda or bias.stride(0) != 1:
+            raise ValueError("bias must be a contiguous CUDA vector of length N")
+        d.bias = bias.data_ptr()
+        d.bias_dtype = _dt(bias)
+    if activation not in (None, "none", "gelu"):
+        raise ValueError(f"unsupported activation {activation!r} (None or 'gelu')")
+    d.activation = _lib.ACT_GELU if activation == "gelu" else _lib.ACT_NONE
     return d
 
 

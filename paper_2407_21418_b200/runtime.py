@@ -79,6 +79,8 @@ class Planner:
         self.coeffs = coeffs or SiaCoeffs()
         self.threads = threads
         self._cache: dict[tuple, PlanRecord] = {}
+        self._exe_cache: dict[tuple, Executable] = {}  # insertion-ordered LRU of lowered tables
+        self.exe_cache_size = 32
         self._lock = threading.Lock()
 
     def _key(self, inst: WorkloadInstance) -> tuple:
@@ -123,8 +125,28 @@ class Planner:
 
     # ---------------------------------------------------------------- ops
 
-    def dense(self, A, B, b_layout: str = "kn", out=None, stream=None):
-        """C = A @ B (B as [K,N] for "kn", as nn.Linear weight [N,K] for "nk")."""
+    def _launch(self, rec, A, B, out, b_layout, bias=None, activation=None, stream=None):
+        """Launch one planned problem through a small cache of lowered tables
+        (keyed by the buffers: TMA descriptors embed their addresses). Cached
+        tables keep their buffers alive, so a key is never reused by another
+        tensor at the same address while cached."""
+        key = tuple((t.data_ptr(), tuple(t.shape), tuple(t.stride()), t.dtype) if t is not None else None
+                    for t in (A, B, out, bias)) + (b_layout, activation, id(rec))
+        with self._lock:
+            ex = self._exe_cache.pop(key, None)
+        if ex is None:
+            ex = Executable([gemm_desc(A, B, out, b_layout, bias=bias, activation=activation)], [rec.program],
+                            (A, B, out, bias, rec))
+        ex.launch(stream)
+        with self._lock:
+            self._exe_cache[key] = ex
+            while len(self._exe_cache) > self.exe_cache_size:
+                self._exe_cache.pop(next(iter(self._exe_cache)))
+        return out
+
+    def dense(self, A, B, b_layout: str = "kn", out=None, stream=None, bias=None, activation=None):
+        """C = act(A @ B + bias) (B as [K,N] for "kn", as nn.Linear weight [N,K]
+        for "nk"); bias [N] and activation ("gelu") are fused into the epilogue."""
         import torch
 
         M, K = A.shape
@@ -135,8 +157,7 @@ class Planner:
         rec = planner.plan([inst])[0]
         if out is None:
             out = torch.empty(M, N, dtype=torch.float32 if fp32 else torch.bfloat16, device=A.device)
-        Executable([gemm_desc(A, B, out, b_layout)], [rec.program], (A, B, out)).launch(stream)
-        return out
+        return self._launch(rec, A, B, out, b_layout, bias, activation, stream)
 
     def bmm(self, A, B, b_layout: str = "kn", dynamic=("i", "j"), out=None, stream=None):
         import torch
@@ -146,8 +167,7 @@ class Planner:
         rec = self.plan([bmm_instance(b, M, N, K, dynamic)])[0]
         if out is None:
             out = torch.empty(b, M, N, dtype=torch.bfloat16, device=A.device)
-        Executable([gemm_desc(A, B, out, b_layout)], [rec.program], (A, B, out)).launch(stream)
-        return out
+        return self._launch(rec, A, B, out, b_layout, stream=stream)
 
     # ---------------------------------------------------------------- persistence
 

@@ -120,3 +120,38 @@ def test_c4_sweep_sample_one_table(cuda, planner):
         assert err.item() < 1e-2, x.shape
         if x.shape.flops < 2e9:
             assert rel(x.C, ss.reference_outputs(i)) < 2e-2, x.shape
+
+
+@pytest.mark.parametrize("M", [1, 37, 160, 1024, 2116])
+@pytest.mark.parametrize("act", [None, "gelu"])
+@pytest.mark.parametrize("bias_dtype", [torch.bfloat16, torch.float32, None])
+def test_dense_fused_bias_gelu(cuda, planner, M, act, bias_dtype):
+    """f-3: Dense + bias (+ GELU, erf form) fused into the epilogue, on every
+    epilogue path (TMA stores, predicated stores, split-K reduction) vs torch."""
+    import torch.nn.functional as F
+
+    N, K = 3072, 768
+    g = torch.Generator(device=cuda).manual_seed(M)
+    A = (torch.rand(M, K, device=cuda, generator=g) * 2 - 1).bfloat16()
+    W = (torch.rand(N, K, device=cuda, generator=g) * 2 - 1).bfloat16() * 0.05
+    bias = None if bias_dtype is None else (torch.rand(N, device=cuda, generator=g) * 2 - 1).to(bias_dtype)
+    C = planner.dense(A, W, b_layout="nk", bias=bias, activation=act)
+    torch.cuda.synchronize()
+    ref = A.double() @ W.double().t()
+    if bias is not None:
+        ref = ref + bias.double()
+    if act == "gelu":
+        ref = F.gelu(ref)
+    assert rel(C, ref) < 2e-2
+
+
+def test_fp32_ffma_fused_bias_gelu(cuda, planner):
+    import torch.nn.functional as F
+
+    g = torch.Generator(device=cuda).manual_seed(3)
+    A = torch.rand(53, 768, device=cuda, generator=g) * 2 - 1
+    B = torch.rand(768, 768, device=cuda, generator=g) * 2 - 1
+    bias = torch.rand(768, device=cuda, generator=g)
+    C = planner.dense(A, B, b_layout="kn", bias=bias, activation="gelu")
+    torch.cuda.synchronize()
+    assert rel(C, F.gelu(A.double() @ B.double() + bias.double())) < 1e-5
