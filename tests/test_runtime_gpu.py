@@ -155,3 +155,25 @@ def test_fp32_ffma_fused_bias_gelu(cuda, planner):
     C = planner.dense(A, B, b_layout="kn", bias=bias, activation="gelu")
     torch.cuda.synchronize()
     assert rel(C, F.gelu(A.double() @ B.double() + bias.double())) < 1e-5
+
+
+@pytest.mark.parametrize("T", [5, 38, 128])
+def test_bert_encoder_layer_module_swap(cuda, planner, T):
+    """f-3 module swap: a torch TransformerEncoderLayer (BERT-base layout,
+    GELU, post-norm) vs the same layer with its six GEMMs on the executor
+    (fused bias / GELU epilogues, attention BMMs batched over heads)."""
+    from paper_2407_21418_b200.bert import EncoderLayer
+
+    torch.manual_seed(T)
+    layer = torch.nn.TransformerEncoderLayer(768, 12, 3072, dropout=0.0, activation="gelu", batch_first=True,
+                                             device=cuda).eval()
+    with torch.no_grad():
+        for p in layer.parameters():  # bf16-representable weights: the comparison isolates the executor
+            p.copy_(p.bfloat16().float())
+    x = (torch.randn(4, T, 768, device=cuda)).bfloat16()
+    with torch.no_grad():
+        ref = layer(x.float())
+    ours = EncoderLayer.from_torch(layer, planner)(x)
+    torch.cuda.synchronize()
+    err = ((ours.float() - ref).abs().max() / ref.abs().max()).item()
+    assert err < 3e-2, err
