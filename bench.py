@@ -297,14 +297,20 @@ def run_ours(args, rank, world, local):
     bound = "tensor" if t_tc >= t_hbm else "hbm"
     if bound == "tensor":
         achieved = flops_rank / (t_step_ms * 1e-3) / 1e12
-        roof = {"bound": "tensor", "achieved": achieved, "peak": peaks["bf16_tflops"], "unit": "TFLOP/s",
-                "frac": achieved / peaks["bf16_tflops"]}
+        # the timed region is a long, power-capped run (>= 1 s of back-to-back
+        # steps): its denominator is the sustained cuBLAS figure; the burst
+        # figure is reported beside it
+        sus = peaks.get("bf16_tflops_sustained") or peaks["bf16_tflops"]
+        roof = {"bound": "tensor", "achieved": achieved, "peak": sus, "unit": "TFLOP/s",
+                "frac": achieved / sus, "peak_burst": peaks["bf16_tflops"],
+                "frac_of_burst": achieved / peaks["bf16_tflops"]}
     else:
         achieved = bytes_rank / (t_step_ms * 1e-3) / 1e9
         roof = {"bound": "hbm", "achieved": achieved, "peak": peaks["hbm_gbs"], "unit": "GB/s",
                 "frac": achieved / peaks["hbm_gbs"]}
     roof["traffic"] = load_traffic("c1_step")
-    roof["peak_source"] = peaks["source"] + " (MEASURED_PEAKS.json burst)" if peaks["source"] == "measured" else "fallback"
+    roof["peak_source"] = (peaks["source"] + (" (MEASURED_PEAKS.json: sustained for tensor-bound, hbm_gbs for hbm-bound)"
+                                              if peaks["source"] == "measured" else ""))
     roof["algorithmic_flops_per_launch"] = flops_rank
     roof["algorithmic_bytes_per_launch"] = bytes_rank
 
