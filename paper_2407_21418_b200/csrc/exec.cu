@@ -584,6 +584,34 @@ static void upload(ExecImpl& I) {
       }
     }
   }
+  // Interleave long (MMA/TMA-bound, e.g. Dense) and short (latency-bound,
+  // e.g. attention BMM) items in rounds of one item per CTA, so each CTA
+  // alternates them: a short item's load -> MMA -> epilogue chain then hides
+  // behind the neighbouring long items instead of forming a serial tail.
+  {
+    const char* env_il = std::getenv("FTB_INTERLEAVE");
+    int sms_here = device_sms();
+    if (sms_here <= 0) sms_here = 148;
+    auto cost = [](const TcWork& t) { return static_cast<int64_t>(t.num_kb) * std::max(kMmaFloorN, t.n_mma); };
+    std::vector<TcWork> lng, shrt;
+    for (const TcWork& t : tw) (cost(t) >= 4 * kMmaFloorN ? lng : shrt).push_back(t);
+    if (!(env_il && env_il[0] == '0') && !lng.empty() && !shrt.empty()) {
+      std::vector<TcWork> mix;
+      mix.reserve(tw.size());
+      size_t a = 0, b = 0;
+      const double ratio = static_cast<double>(shrt.size()) / static_cast<double>(lng.size());
+      double owed = 0.0;
+      while (a < lng.size() || b < shrt.size()) {
+        const size_t na = std::min(lng.size() - a, static_cast<size_t>(sms_here));
+        for (size_t q = 0; q < na; ++q) mix.push_back(lng[a++]);
+        owed += na ? na * ratio : static_cast<double>(shrt.size() - b);
+        size_t nb = std::min(shrt.size() - b, static_cast<size_t>(owed));
+        owed -= static_cast<double>(nb);
+        for (size_t q = 0; q < nb; ++q) mix.push_back(shrt[b++]);
+      }
+      tw.swap(mix);
+    }
+  }
   I.n_singles = static_cast<int64_t>(tw.size());
   I.n_pairs = static_cast<int64_t>(pairs.size());
   if (!tw.empty()) {
