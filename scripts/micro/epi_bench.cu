@@ -15,7 +15,7 @@ struct Maps { CUtensorMap a; CUtensorMap b; CUtensorMap c; };
 
 template <int PAIR>
 __global__ void __launch_bounds__(192, 1) epi_kernel(const __grid_constant__ Maps maps, int items, int KB, int S,
-                                                     int N, unsigned long long* out, int epi, __nv_bfloat16* C, int dbg) {
+                                                     int N, unsigned long long* out, int epi, __nv_bfloat16* C, int dbg, int real) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   const int b_rows = PAIR ? N / 2 : N;
@@ -47,16 +47,18 @@ __global__ void __launch_bounds__(192, 1) epi_kernel(const __grid_constant__ Map
         mbar_wait(&empty[ps], ph ^ 1);
         uint8_t* dst = smem + ps * stage_bytes;
         int k0 = kb * 64;
-        int row = ((cid * 7 + item) % 14) * 256 + rank * 128;
+        const int wi = cid + item * (PAIR ? (int)(gridDim.x / 2) : (int)gridDim.x);
+        int row = real ? (wi / 16 % 16) * 256 + rank * 128 : ((cid * 7 + item) % 14) * 256 + rank * 128;
+        const int brow = real ? (wi % 16) * 256 + rank * b_rows : ((cid * 3 + item) % 14) * 256 + rank * b_rows;
         if (PAIR) {
           uint32_t fb = smem_addr(&full[ps]) & 0xFEFFFFFFu;
           if (rank == 0) mbar_arrive_expect_tx(&full[ps], 2 * stage_bytes);
           tma_load_3d_pair(dst, &maps.a, fb, k0, row, 0);
-          tma_load_3d_pair(dst + a_bytes, &maps.b, fb, k0, ((cid * 3 + item) % 14) * 256 + rank * b_rows, 0);
+          tma_load_3d_pair(dst + a_bytes, &maps.b, fb, k0, brow, 0);
         } else {
           mbar_arrive_expect_tx(&full[ps], stage_bytes);
           tma_load_3d(dst, &maps.a, &full[ps], k0, row, 0);
-          tma_load_3d(dst + a_bytes, &maps.b, &full[ps], k0, ((cid * 3 + item) % 14) * 256, 0);
+          tma_load_3d(dst + a_bytes, &maps.b, &full[ps], k0, real ? (wi % 16) * 256 : ((cid * 3 + item) % 14) * 256, 0);
         }
         if (++ps == S) { ps = 0; ph ^= 1; }
       }
@@ -181,17 +183,19 @@ int main() {
   const int64_t K = 4096, R = 4096;
   __nv_bfloat16* buf; cudaMalloc(&buf, K * R * 2);
   fill<<<1024, 256>>>(buf, K * R);
+  __nv_bfloat16* buf2; cudaMalloc(&buf2, K * R * 2);
+  fill<<<1024, 256>>>(buf2, K * R);
   __nv_bfloat16* C; cudaMalloc(&C, 148 * 128 * 256 * 2);
   unsigned long long* out; cudaMalloc(&out, 148 * 8);
   const int ctas = 148;
-  struct Cfg { int pair, N, S, KB, items, epi; } cfgs[] = {
-      {0, 256, 4, 12, 64, 3}, {0, 256, 4, 12, 64, 2}, {0, 256, 4, 12, 64, 1}, {0, 128, 6, 12, 64, 3},
+  struct Cfg { int pair, N, S, KB, items, epi, real = 0; } cfgs[] = {
+      {1, 256, 6, 64, 4, 3, 0}, {1, 256, 6, 64, 4, 3, 1}, {0, 256, 4, 64, 4, 3, 0}, {0, 256, 4, 64, 4, 3, 1},
       };
   int dbg = 0;
   for (auto& c : cfgs) {
     Maps m;
     make(&m.a, buf, K, R, 128);
-    make(&m.b, buf, K, R, c.pair ? c.N / 2 : c.N);
+    make(&m.b, c.real ? buf2 : buf, K, R, c.pair ? c.N / 2 : c.N);
     {
       cuuint64_t dims[3] = {256, 148 * 128, 1};
       cuuint64_t strides[2] = {256 * 2, 148 * 128 * 256 * 2};
@@ -211,9 +215,9 @@ int main() {
     cudaError_t e;
     auto launch = [&](int items) {
       if (!c.pair) { cudaFuncSetAttribute(epi_kernel<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-        e = cudaLaunchKernelEx(&lc, epi_kernel<0>, m, items, c.KB, c.S, c.N, out, c.epi, C, dbg); }
+        e = cudaLaunchKernelEx(&lc, epi_kernel<0>, m, items, c.KB, c.S, c.N, out, c.epi, C, dbg, c.real); }
       else { cudaFuncSetAttribute(epi_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-        e = cudaLaunchKernelEx(&lc, epi_kernel<1>, m, items, c.KB, c.S, c.N, out, c.epi, C, dbg); }
+        e = cudaLaunchKernelEx(&lc, epi_kernel<1>, m, items, c.KB, c.S, c.N, out, c.epi, C, dbg, c.real); }
     };
     dbg = 0;
     launch(4); cudaDeviceSynchronize();

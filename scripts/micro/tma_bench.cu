@@ -40,7 +40,14 @@ __global__ void __launch_bounds__(192, 1) tma_kernel(const __grid_constant__ Map
       int k0 = (it % 64) * 64;
       const Maps& maps = (gmaps && ndesc > 1) ? gmaps[(it + blockIdx.x) % ndesc] : maps0;
       int row = big ? ((blockIdx.x * 64 + it / 64) * 256) % (R_rows - 512) : ((blockIdx.x * 7 + it / 64) % 16) * 256;
-      if (MODE == 4) {
+      if (MODE == 5) {
+        mbar_arrive_expect_tx(&full[ps], (a_rows + b_rows) * 128);
+        // a_rows = 256 rows of smem = 128 rows x 2 K blocks in one box
+        asm volatile("cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4, %5}], [%2];"
+                     :: "r"(smem_addr(dst)), "l"(reinterpret_cast<uint64_t>(&maps.a)), "r"(smem_addr(&full[ps])),
+                        "r"(0), "r"(row), "r"((k0 / 64) % 32) : "memory");
+        if (b_rows) tma_load_3d(dst + a_rows * 128, &maps.b, &full[ps], k0, row + 128, 0);
+      } else if (MODE == 4) {
         // own lane box (a_rows) + half of a 2*b_rows col tile, multicast to both CTAs
         mbar_arrive_expect_tx(&full[ps], (a_rows + 2 * b_rows) * 128);
         tma_load_3d(dst, &maps.a, &full[ps], k0, row, 0);
@@ -109,7 +116,7 @@ int main() {
   int ctas = 148, iters = 2000;
   Maps* dmaps; cudaMalloc(&dmaps, 512 * sizeof(Maps));
   struct Cfg { int mode, a, b, S; const char* name; int gm = 0; int spin = 0; int big = 0; } cfgs[] = {
-      {0, 128, 256, 4, "BIG single 128+256 S4", 0, 0, 1}, {1, 128, 128, 6, "BIG pair 128+128 S6", 0, 0, 1}, {2, 128, 128, 6, "BIG cluster2 plain 128+128 S6", 0, 0, 1}, {0, 128, 128, 6, "BIG single 128+128 S6", 0, 0, 1}, {0, 128, 256, 4, "single 128+256 S4 (same ingest)", 0}, {0, 128, 128, 6, "GMEM-desc single 128+128 S6", 1}, {0, 128, 128, 6, "GMEM 8 descs", 8}, {0, 128, 128, 6, "GMEM 64 descs", 64}, {0, 128, 128, 6, "GMEM 512 descs", 512}, {0, 128, 128, 6, "single + 4 spinning warps", 0, 1}, {0, 128, 256, 4, "single 128+256 + 4 spinning warps", 0, 1}, {1, 128, 128, 6, "GMEM-desc pair 128+128 S6", 1},
+      {5, 256, 0, 6, "ONE 3-D box 128x2kb (32KB) S6"}, {0, 128, 128, 6, "TWO boxes 128+128 (32KB) S6"}, {0, 256, 0, 6, "ONE box 256 rows (32KB) S6"}, {5, 256, 256, 4, "3-D box 2kb + 256 box (64KB) S4"}, {1, 128, 128, 6, "BIG pair 128+128 S6", 0, 0, 1}, {2, 128, 128, 6, "BIG cluster2 plain 128+128 S6", 0, 0, 1}, {0, 128, 128, 6, "BIG single 128+128 S6", 0, 0, 1}, {0, 128, 256, 4, "single 128+256 S4 (same ingest)", 0}, {0, 128, 128, 6, "GMEM-desc single 128+128 S6", 1}, {0, 128, 128, 6, "GMEM 8 descs", 8}, {0, 128, 128, 6, "GMEM 64 descs", 64}, {0, 128, 128, 6, "GMEM 512 descs", 512}, {0, 128, 128, 6, "single + 4 spinning warps", 0, 1}, {0, 128, 256, 4, "single 128+256 + 4 spinning warps", 0, 1}, {1, 128, 128, 6, "GMEM-desc pair 128+128 S6", 1},
       {0, 128, 256, 4, "single 128+256 S4"}, {0, 128, 128, 6, "single 128+128 S6"}, {0, 128, 64, 8, "single 128+64 S8"},
       {0, 128, 0, 8, "single 128 only S8"}, {0, 256, 0, 6, "single 256 only S6"},
       {1, 128, 128, 6, "pair(cta_group::2) 128+128 S6"}, {1, 128, 64, 8, "pair 128+64 S8"}, {3, 128, 128, 6, "pair masked-bar 128+128 S6"},
@@ -117,6 +124,14 @@ int main() {
   };
   for (auto& c : cfgs) {
     Maps m;
+    if (c.mode == 5) {  // 3-D view {64 (k inner), rows, K/64 (k outer)} with box {64, 128, 2}
+      cuuint64_t dims[3] = {64, (cuuint64_t)R, (cuuint64_t)(K / 64)};
+      cuuint64_t strides[2] = {(cuuint64_t)K * 2, 128};
+      cuuint32_t box[3] = {64, 128, 2}, es[3] = {1, 1, 1};
+      CUresult r = enc()(&m.a, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, buf, dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+            CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+      if (r) printf("encode 3d-k failed %d\n", r);
+    } else
     make(&m.a, buf, K, R, c.a > 0 ? (c.a > 256 ? 256 : c.a) : 64);
     make(&m.b, buf, K, R, c.b > 0 ? c.b : 64);
     for (int d = 0; d < 512; ++d) cudaMemcpy(dmaps + d, &m, sizeof(Maps), cudaMemcpyHostToDevice);
@@ -133,6 +148,8 @@ int main() {
         e = cudaLaunchKernelEx(&lc, tma_kernel<0>, m, it, c.S, c.a, c.b, out, c.gm ? dmaps : nullptr, c.gm, c.big, (int)R); }
       else if (c.mode == 3) { cudaFuncSetAttribute(tma_kernel<1, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
         e = cudaLaunchKernelEx(&lc, tma_kernel<1, 1>, m, it, c.S, c.a, c.b, out, c.gm ? dmaps : nullptr, c.gm, c.big, (int)R); }
+      else if (c.mode == 5) { cudaFuncSetAttribute(tma_kernel<5>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+        e = cudaLaunchKernelEx(&lc, tma_kernel<5>, m, it, c.S, c.a, c.b, out, c.gm ? dmaps : nullptr, c.gm, c.big, (int)R); }
       else if (c.mode == 4) { cudaFuncSetAttribute(tma_kernel<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
         e = cudaLaunchKernelEx(&lc, tma_kernel<4>, m, it, c.S, c.a, c.b, out, c.gm ? dmaps : nullptr, c.gm, c.big, (int)R); }
       else if (c.mode == 1) { cudaFuncSetAttribute(tma_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
