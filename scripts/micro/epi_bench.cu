@@ -14,8 +14,9 @@ using namespace ftb;
 struct Maps { CUtensorMap a; CUtensorMap b; CUtensorMap c; };
 
 template <int PAIR>
-__global__ void __launch_bounds__(192, 1) epi_kernel(const __grid_constant__ Maps maps, int items, int KB, int S,
-                                                     int N, unsigned long long* out, int epi, __nv_bfloat16* C, int dbg, int real) {
+__global__ void __launch_bounds__(192, 1) epi_kernel(const __grid_constant__ Maps maps_p, int items, int KB, int S,
+                                                     int N, unsigned long long* out, int epi, __nv_bfloat16* C, int dbg, int real, const Maps* gmaps) {
+  const Maps& maps = gmaps ? *gmaps : maps_p;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   const int b_rows = PAIR ? N / 2 : N;
@@ -47,7 +48,7 @@ __global__ void __launch_bounds__(192, 1) epi_kernel(const __grid_constant__ Map
         mbar_wait(&empty[ps], ph ^ 1);
         uint8_t* dst = smem + ps * stage_bytes;
         int k0 = kb * 64;
-        const int wi = cid + item * (PAIR ? (int)(gridDim.x / 2) : (int)gridDim.x);
+        const int wi = (cid + item * (PAIR ? (int)(gridDim.x / 2) : (int)gridDim.x)) % 256;
         int row = real ? (wi / 16 % 16) * 256 + rank * 128 : ((cid * 7 + item) % 14) * 256 + rank * 128;
         const int brow = real ? (wi % 16) * 256 + rank * b_rows : ((cid * 3 + item) % 14) * 256 + rank * b_rows;
         if (PAIR) {
@@ -188,10 +189,11 @@ int main() {
   __nv_bfloat16* C; cudaMalloc(&C, 148 * 128 * 256 * 2);
   unsigned long long* out; cudaMalloc(&out, 148 * 8);
   const int ctas = 148;
-  struct Cfg { int pair, N, S, KB, items, epi, real = 0; } cfgs[] = {
-      {1, 256, 6, 64, 4, 3, 0}, {1, 256, 6, 64, 4, 3, 1}, {0, 256, 4, 64, 4, 3, 0}, {0, 256, 4, 64, 4, 3, 1},
+  struct Cfg { int pair, N, S, KB, items, epi, real = 0, gm = 0; } cfgs[] = {
+      {1, 256, 6, 64, 64, 3, 1, 1}, {0, 256, 4, 64, 64, 3, 1, 1}, {1, 256, 6, 64, 64, 3, 1, 1}, {0, 256, 4, 64, 64, 3, 1, 1},
       };
   int dbg = 0;
+  Maps* dmaps; cudaMalloc(&dmaps, sizeof(Maps));
   for (auto& c : cfgs) {
     Maps m;
     make(&m.a, buf, K, R, 128);
@@ -204,6 +206,7 @@ int main() {
             CU_TENSOR_MAP_SWIZZLE_64B, CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
       if (r) printf("encode C failed %d\n", r);
     }
+    cudaMemcpy(dmaps, &m, sizeof(Maps), cudaMemcpyHostToDevice);
     int b_rows = c.pair ? c.N / 2 : c.N;
     int smem = c.S * (128 + b_rows) * 128 + 2048 + 16384;
     cudaLaunchConfig_t lc = {};
@@ -215,9 +218,9 @@ int main() {
     cudaError_t e;
     auto launch = [&](int items) {
       if (!c.pair) { cudaFuncSetAttribute(epi_kernel<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-        e = cudaLaunchKernelEx(&lc, epi_kernel<0>, m, items, c.KB, c.S, c.N, out, c.epi, C, dbg, c.real); }
+        e = cudaLaunchKernelEx(&lc, epi_kernel<0>, m, items, c.KB, c.S, c.N, out, c.epi, C, dbg, c.real, c.gm ? dmaps : nullptr); }
       else { cudaFuncSetAttribute(epi_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-        e = cudaLaunchKernelEx(&lc, epi_kernel<1>, m, items, c.KB, c.S, c.N, out, c.epi, C, dbg, c.real); }
+        e = cudaLaunchKernelEx(&lc, epi_kernel<1>, m, items, c.KB, c.S, c.N, out, c.epi, C, dbg, c.real, c.gm ? dmaps : nullptr); }
     };
     dbg = 0;
     launch(4); cudaDeviceSynchronize();
@@ -229,8 +232,8 @@ int main() {
     double mc = 0; for (auto v : cyc) mc += v; mc /= ctas;
     double kbs = (double)c.items * c.KB;
     double flops = 2.0 * 128 * c.N * 64 * kbs * ctas;
-    printf("%s N=%d S=%d KB=%d items=%d epi=%d err=%d: %.3f ms, %.0f clk/kblock (ideal %d), %.0f TF/s, clk %.2f GHz\n",
-           c.pair ? "pair  " : "single", c.N, c.S, c.KB, c.items, c.epi, (int)e, ms, mc / kbs, 2 * c.N,
+    printf("%s gm=%d N=%d S=%d KB=%d items=%d epi=%d err=%d: %.3f ms, %.0f clk/kblock (ideal %d), %.0f TF/s, clk %.2f GHz\n",
+           c.pair ? "pair  " : "single", c.gm, c.N, c.S, c.KB, c.items, c.epi, (int)e, ms, mc / kbs, 2 * c.N,
            flops / (ms * 1e-3) / 1e12, mc / (ms * 1e6));
   }
   return 0;
