@@ -543,12 +543,52 @@ static void upload(ExecImpl& I) {
   // kMaxSplit items; partials meet in an fp32 workspace and the last warp to
   // arrive per lane quadrant reduces and stores (kernel_tc.cu). Tables that
   // already fill the GPU (the grouped C1 step) are left alone.
+  // Column split: a table with fewer than half as many items as SMs runs one
+  // wave whose length is one item's K loop; a 256-column item's K block costs
+  // ~550 clk (smem-port bound: 48 KiB TMA write + 48 KiB MMA read), a
+  // 128-column one ~350 clk. Halving wide items along the column axis
+  // shortens the wave without changing any output bit (same per-element
+  // K order).
+  {
+    int sms_here = device_sms();
+    if (sms_here <= 0) sms_here = 148;
+    const char* env_cs = std::getenv("FTB_COLSPLIT");
+    const bool cs_on = !(env_cs && env_cs[0] == '0') && !pairing;
+    int64_t wide = 0;
+    for (const TcWork& t : tw) wide += (!t.pack && t.n_mma > 128 && t.col_len > 128) ? 1 : 0;
+    if (cs_on && wide > 0 && static_cast<int64_t>(tw.size()) + wide <= sms_here) {
+      std::vector<TcWork> cs;
+      cs.reserve(tw.size() + wide);
+      for (const TcWork& t : tw) {
+        if (t.pack || t.n_mma <= 128 || t.col_len <= 128) {
+          cs.push_back(t);
+          continue;
+        }
+        const bool col_mn = (t.flags & kFlagColMN) != 0;
+        TcWork a = t, b = t;
+        a.col_len = 128;
+        a.n_mma = 128;
+        b.col0 = t.col0 + 128;
+        b.col_len = t.col_len - 128;
+        b.n_mma = static_cast<int32_t>(round_up(b.col_len, col_mn ? 128 : 32));
+        cs.push_back(a);
+        cs.push_back(b);
+      }
+      tw.swap(cs);
+      max_n = 16;
+      for (const TcWork& t : tw) max_n = std::max(max_n, t.n_mma);
+    }
+  }
   {
     int sms_here = device_sms();
     if (sms_here <= 0) sms_here = 148;
     const char* env_sk = std::getenv("FTB_SPLITK");
     const bool split_on = !(env_sk && env_sk[0] == '0') && !pairing;
     const int64_t n_items = static_cast<int64_t>(tw.size());
+    const char* env_mk = std::getenv("FTB_SPLIT_MINKB");
+    const int split_min_kb = env_mk ? std::max(1, std::atoi(env_mk)) : 8;
+    const char* env_w = std::getenv("FTB_SPLIT_WIDE");
+    const bool split_wide = env_w && env_w[0] == '1';
     if (split_on && n_items > 0 && n_items * 2 <= sms_here) {
       const int target = static_cast<int>(std::min<int64_t>(kMaxSplit, sms_here / n_items));
       std::vector<TcWork> split;
@@ -558,7 +598,7 @@ static void upload(ExecImpl& I) {
         // round trip (128 x n_mma x 8 B) must stay small next to the operand
         // bytes a split saves (measured: C3 M<=127 22 -> 18 us, M=256 n=256
         // tiles 23 -> 28 us when split)
-        const int s_t = t.n_mma <= 128 ? std::min(target, t.num_kb / 8) : 1;
+        const int s_t = (t.n_mma <= 128 || split_wide) ? std::min(target, t.num_kb / split_min_kb) : 1;
         if (t.pack || s_t < 2) {
           split.push_back(t);
           continue;
@@ -576,10 +616,12 @@ static void upload(ExecImpl& I) {
           split.push_back(u);
         }
       }
-      if (tiles > 0) {
+      // the split epilogue's all-splits rendezvous needs every item resident
+      // at once: one item per CTA, at most one CTA per SM
+      if (tiles > 0 && static_cast<int64_t>(split.size()) <= sms_here) {
         FTB_CUDA(cudaMalloc(&I.d_split_ws, sizeof(float) * static_cast<size_t>(tiles) * kSplitTileFloats));
-        FTB_CUDA(cudaMalloc(&I.d_split_cnt, sizeof(int32_t) * 4 * tiles));
-        FTB_CUDA(cudaMemset(I.d_split_cnt, 0, sizeof(int32_t) * 4 * tiles));
+        FTB_CUDA(cudaMalloc(&I.d_split_cnt, sizeof(int32_t) * 8 * tiles));
+        FTB_CUDA(cudaMemset(I.d_split_cnt, 0, sizeof(int32_t) * 8 * tiles));
         tw.swap(split);
       }
     }

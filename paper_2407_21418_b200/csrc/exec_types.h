@@ -136,7 +136,7 @@ struct TcConfig {
   int32_t acc_cols;        // columns per slot (512 / n_acc)
   unsigned long long* trace;  // optional: per-CTA phase timestamps (debug)
   float* split_ws;            // split-K partials [tile][split][128][256] fp32
-  int32_t* split_cnt;         // split-K arrivals [tile][4 lane quadrants]
+  int32_t* split_cnt;         // split-K counters [tile][arrive, depart][4 lane quadrants]
 };
 constexpr int kTraceItems = 16;   // items traced per CTA
 constexpr int kTraceEvents = 6;   // see kernel_tc.cu

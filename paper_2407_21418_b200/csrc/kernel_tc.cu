@@ -98,22 +98,44 @@ __device__ __forceinline__ void split_epilogue(const TcConfig& cfg, const TcWork
   release();  // TMEM no longer needed
   __threadfence();
   __syncwarp();
-  int32_t* cnt = cfg.split_cnt + tile * 4 + quad;
-  int arrived = 0;
-  if (lane == 0) arrived = atomicAdd(cnt, 1);
-  arrived = __shfl_sync(0xffffffffu, arrived, 0);
-  if (arrived != nsplit - 1) return;  // not the last split of this quadrant
+  // All splits of a tile are resident at once (split-K is only planned for
+  // tables of <= one item per SM, exec.cu), so every split warp of this
+  // quadrant waits for the others' partials and then reduces its share of
+  // the 32-column chunks: the reduction runs on nsplit warps in parallel
+  // instead of serially on the last to arrive.
+  int32_t* arrive = cfg.split_cnt + tile * 8 + quad;
+  int32_t* depart = arrive + 4;
+  if (lane == 0) {
+    atomicAdd(arrive, 1);
+    while (ld_acquire_gpu(arrive) < nsplit) __nanosleep(32);
+  }
+  __syncwarp();
   __threadfence();
-  if (lane == 0) *cnt = 0;  // re-arm for the next launch (stream order separates launches)
-  if (lane_base >= it.lane_len) return;
   float* tb = reinterpret_cast<float*>(region);
   if (lane == 0) bulk_wait_read<0>();  // the transpose tile aliases this warp's store boxes
   __syncwarp();
-  for (int c0 = 0; c0 < it.col_len; c0 += 32) {
+  const int c_first = me * 32;
+  const int c_step = nsplit * 32;
+  for (int c0 = (lane_base < it.lane_len) ? c_first : it.col_len; c0 < it.col_len; c0 += c_step) {
     float v[32];
 #pragma unroll
     for (int e = 0; e < 32; ++e) v[e] = 0.f;
-    for (int sp = 0; sp < nsplit; ++sp) {  // fixed order: deterministic sum
+    int sp = 0;
+    for (; sp + 3 <= nsplit; sp += 3) {  // three partials in flight; fixed order: deterministic sum
+      const float* s0 = part(sp, c0);
+      const float* s1 = part(sp + 1, c0);
+      const float* s2 = part(sp + 2, c0);
+      float a[32], b[32], c[32];
+#pragma unroll
+      for (int e = 0; e < 32; ++e) {
+        a[e] = __ldcg(s0 + e * 32);
+        b[e] = __ldcg(s1 + e * 32);
+        c[e] = __ldcg(s2 + e * 32);
+      }
+#pragma unroll
+      for (int e = 0; e < 32; ++e) v[e] = ((v[e] + a[e]) + b[e]) + c[e];
+    }
+    for (; sp < nsplit; ++sp) {
       const float* src = part(sp, c0);
 #pragma unroll
       for (int e = 0; e < 32; ++e) v[e] += __ldcg(src + e * 32);
@@ -132,6 +154,13 @@ __device__ __forceinline__ void split_epilogue(const TcConfig& cfg, const TcWork
       store_block32(tb, v, true, it.C, it.ldc, it.lane0 + lane_base, it.col0 + c0, nlane, ncol, f32);
     else
       store_block32(tb, v, false, it.C, it.ldc, it.col0 + c0, it.lane0 + lane_base, ncol, nlane, f32);
+  }
+  // the last warp out re-arms both counters for the next launch (stream
+  // order, or griddepcontrol.wait under PDL, separates launches)
+  __syncwarp();
+  if (lane == 0 && atomicAdd(depart, 1) == nsplit - 1) {
+    *arrive = 0;
+    *depart = 0;
   }
 }
 

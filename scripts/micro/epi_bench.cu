@@ -7,6 +7,8 @@
 #include <cuda_runtime.h>
 #include <cuda_bf16.h>
 #include <cstdio>
+#include <cstdlib>
+#include <string>
 #include <cstdint>
 #include <vector>
 #include "../../paper_2407_21418_b200/csrc/ptx.cuh"
@@ -188,10 +190,25 @@ int main() {
   fill<<<1024, 256>>>(buf2, K * R);
   __nv_bfloat16* C; cudaMalloc(&C, 148 * 128 * 256 * 2);
   unsigned long long* out; cudaMalloc(&out, 148 * 8);
-  const int ctas = 148;
-  struct Cfg { int pair, N, S, KB, items, epi, real = 0, gm = 0; } cfgs[] = {
+  const int ctas = getenv("CTAS") ? atoi(getenv("CTAS")) : 148;
+  struct Cfg { int pair, N, S, KB, items, epi, real = 0, gm = 0; };
+  std::vector<Cfg> cfgs = {
       {1, 256, 6, 64, 64, 3, 1, 1}, {0, 256, 4, 64, 64, 3, 1, 1}, {1, 256, 6, 64, 64, 3, 1, 1}, {0, 256, 4, 64, 64, 3, 1, 1},
       };
+  if (const char* env = getenv("CFGS")) {  // "pair,N,S,KB,items,epi;..." (real=1, gm=1)
+    cfgs.clear();
+    std::string all(env);
+    size_t p0 = 0;
+    while (p0 < all.size()) {
+      size_t p1 = all.find(';', p0);
+      if (p1 == std::string::npos) p1 = all.size();
+      Cfg c{};
+      c.real = 1; c.gm = 1;
+      sscanf(all.substr(p0, p1 - p0).c_str(), "%d,%d,%d,%d,%d,%d", &c.pair, &c.N, &c.S, &c.KB, &c.items, &c.epi);
+      cfgs.push_back(c);
+      p0 = p1 + 1;
+    }
+  }
   int dbg = 0;
   Maps* dmaps; cudaMalloc(&dmaps, sizeof(Maps));
   for (auto& c : cfgs) {

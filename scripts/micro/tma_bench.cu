@@ -5,6 +5,7 @@
 #include <cudaTypedefs.h>
 #include <cuda_runtime.h>
 #include <cstdio>
+#include <cstdlib>
 #include <cstdint>
 #include <vector>
 #include "../../paper_2407_21418_b200/csrc/ptx.cuh"
@@ -113,7 +114,7 @@ int main() {
   const int64_t K = 4096, R = 65536;  // 512 MiB: BIG mode streams from HBM
   void* buf; cudaMalloc(&buf, K * R * 2); cudaMemset(buf, 0, K * R * 2);
   unsigned long long* out; cudaMalloc(&out, 148 * 8);
-  int ctas = 148, iters = 2000;
+  int ctas = getenv("CTAS") ? atoi(getenv("CTAS")) : 148, iters = getenv("ITERS") ? atoi(getenv("ITERS")) : 2000;
   Maps* dmaps; cudaMalloc(&dmaps, 512 * sizeof(Maps));
   struct Cfg { int mode, a, b, S; const char* name; int gm = 0; int spin = 0; int big = 0; } cfgs[] = {
       {5, 256, 0, 6, "ONE 3-D box 128x2kb (32KB) S6"}, {0, 128, 128, 6, "TWO boxes 128+128 (32KB) S6"}, {0, 256, 0, 6, "ONE box 256 rows (32KB) S6"}, {5, 256, 256, 4, "3-D box 2kb + 256 box (64KB) S4"}, {1, 128, 128, 6, "BIG pair 128+128 S6", 0, 0, 1}, {2, 128, 128, 6, "BIG cluster2 plain 128+128 S6", 0, 0, 1}, {0, 128, 128, 6, "BIG single 128+128 S6", 0, 0, 1}, {0, 128, 256, 4, "single 128+256 S4 (same ingest)", 0}, {0, 128, 128, 6, "GMEM-desc single 128+128 S6", 1}, {0, 128, 128, 6, "GMEM 8 descs", 8}, {0, 128, 128, 6, "GMEM 64 descs", 64}, {0, 128, 128, 6, "GMEM 512 descs", 512}, {0, 128, 128, 6, "single + 4 spinning warps", 0, 1}, {0, 128, 256, 4, "single 128+256 + 4 spinning warps", 0, 1}, {1, 128, 128, 6, "GMEM-desc pair 128+128 S6", 1},
