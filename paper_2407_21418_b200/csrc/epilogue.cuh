@@ -191,6 +191,23 @@ __device__ __forceinline__ void apply_epi(uint32_t (&r)[32], const EpiOp& op, bo
 // last TMEM read. `region` is the warp's 8 KiB staging area (four 2 KiB TMA
 // boxes or the 32x33 fp32 transpose tile), `ngrp` its running box-group count.
 // `op` (or null): fused bias + activation applied before rounding.
+#ifdef FTB_EPI_TRACE
+// debug: per-CTA epilogue timestamps of warp 4 (lane quadrant 0), first item
+// (a device global, not __shared__: static smem would overflow the 227 KiB opt-in)
+__device__ unsigned long long* ftb_epi_dbg;
+#define FTB_EPI_EV(i)                                                                                   \
+  do {                                                                                                  \
+    unsigned long long* d_ = ftb_epi_dbg ? ftb_epi_dbg + static_cast<size_t>(blockIdx.x) * kTracePerCta \
+                                                + kTraceItems * kTraceEvents + 2 * 40                    \
+                                         : nullptr;                                                      \
+    if (d_ && (threadIdx.x >> 5) == 4 && (threadIdx.x & 31) == 0) d_[i] = clock64();  \
+  } while (0)
+#else
+#define FTB_EPI_EV(i) \
+  do {                \
+  } while (0)
+#endif
+
 template <class Release>
 __device__ __forceinline__ void epilogue_tile(uint8_t* region, uint32_t& ngrp, uint32_t taddr, bool active, bool tma,
                                               bool swap, bool f32, const CUtensorMap* out_map, void* C, int64_t ldc,
@@ -208,6 +225,7 @@ __device__ __forceinline__ void epilogue_tile(uint8_t* region, uint32_t& ngrp, u
         tmem_ld_32x32b_x32(taddr + c0, ra);
         if (two) tmem_ld_32x32b_x32(taddr + c0 + 32, rb);
         tmem_ld_wait();
+        FTB_EPI_EV((c0 >> 6) * 6 + 0);
         if (c0 + 64 >= col_len) {  // last TMEM read of the item
           release();
           released = true;
@@ -219,14 +237,18 @@ __device__ __forceinline__ void epilogue_tile(uint8_t* region, uint32_t& ngrp, u
         uint8_t* box = region + (ngrp & 1) * 4096;
         if (lane == 0) bulk_wait_read<1>();  // the group that last used these boxes has read them
         __syncwarp();
+        FTB_EPI_EV((c0 >> 6) * 6 + 1);
         stage_box_bf16(box, ra, !swap);
         if (two) stage_box_bf16(box + 2048, rb, !swap);
+        FTB_EPI_EV((c0 >> 6) * 6 + 2);
         fence_async_smem();
         __syncwarp();
+        FTB_EPI_EV((c0 >> 6) * 6 + 3);
         if (lane == 0) {
           const int l0 = lane0 + lane_base, k0 = col0 + c0;
           if (!swap) {
             tma_store_3d(out_map, smem_addr(box), k0, l0, batch);
+            FTB_EPI_EV((c0 >> 6) * 6 + 4);
             if (two) tma_store_3d(out_map, smem_addr(box + 2048), k0 + 32, l0, batch);
           } else {
             tma_store_3d(out_map, smem_addr(box), l0, k0, batch);
@@ -234,6 +256,7 @@ __device__ __forceinline__ void epilogue_tile(uint8_t* region, uint32_t& ngrp, u
           }
           bulk_commit();
         }
+        FTB_EPI_EV((c0 >> 6) * 6 + 5);
         ++ngrp;
       }
     } else {

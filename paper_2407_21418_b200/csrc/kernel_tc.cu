@@ -195,6 +195,9 @@ __global__ void __launch_bounds__(kTcThreads, 1)
     fence_barrier_init();
   }
   if (warp == 2) tmem_alloc<kTmemCols>(tmem_holder);
+#ifdef FTB_EPI_TRACE
+  if (threadIdx.x == 0) ftb_epi_dbg = cfg.trace;  // same value from every CTA
+#endif
   tc_fence_before();
   __syncthreads();
   tc_fence_after();

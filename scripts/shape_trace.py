@@ -46,4 +46,10 @@ for spec in os.environ.get("SHAPES", "160 768 768;1376 768 768;160 768 3072").sp
     for c in sorted(set([0, n - 1])):
         print(f"  cta{c} kb issue:", " ".join(f"{v:.2f}" for v in kbr[c, :16, 0]))
         print(f"  cta{c} kb mma  :", " ".join(f"{v:.2f}" for v in kbr[c, :16, 1]))
+    if os.environ.get("EPI"):
+        ep = kb[:n, 40:46, :].reshape(n, 12).astype(np.int64)
+        d = np.diff(ep, axis=1)
+        print("  epi clk deltas (ld->waitread, ->staged, ->fenced, ->store0, ->store1+commit, ->ld1, ...) median over CTAs:",
+              np.median(d, axis=0).astype(int).tolist())
+        print("  rel - epi per CTA p50:", f"{np.median(rel[:n,0,5]-rel[:n,0,4]):.2f}")
     ex.close()
