@@ -205,10 +205,11 @@ __global__ void __launch_bounds__(kTcThreads, 1)
   const uint32_t smem_u32 = smem_addr(smem);
   const uint32_t lane_u32 = smem_addr(lane_buf), col_u32 = smem_addr(col_buf);
   // Programmatic dependent launch: everything above (barrier init, TMEM
-  // allocation) overlaps the previous grid's tail; operands and outputs are
-  // touched only after it has completed. Dependents may launch right away —
-  // they in turn wait here for this grid.
-  griddep_wait();
+  // allocation) and the producer's work-record fetch and descriptor prefetch
+  // (host-written at executable creation) overlap the previous grid's tail.
+  // Only the producer waits for that grid: every operand load is issued after
+  // its wait, and every output write is causally after an operand load.
+  // Dependents may launch right away — they in turn wait for this grid.
   griddep_launch_dependents();
   const int G = gridDim.x;
 
@@ -230,6 +231,11 @@ __global__ void __launch_bounds__(kTcThreads, 1)
     if (static_cast<int>(blockIdx.x) < n_work) cur = bcast_work(fetch_work_word(work, blockIdx.x));
     if (static_cast<int>(blockIdx.x) + G < n_work) nxt = bcast_work(fetch_work_word(work, blockIdx.x + G));
     if (static_cast<int>(blockIdx.x) + 2 * G < n_work) pend = fetch_work_word(work, blockIdx.x + 2 * G);
+    if (lane == 0 && static_cast<int>(blockIdx.x) < n_work) {
+      tma_prefetch_desc(&cur.maps->lane);
+      tma_prefetch_desc(&cur.maps->col[0]);
+    }
+    griddep_wait();
     for (int w = blockIdx.x; w < n_work; w += G, ++local) {
       const TcWork it = cur;
       if (lane == 0) {
