@@ -4,6 +4,9 @@
 #include <cudaTypedefs.h>
 #include <cuda_runtime.h>
 #include <cstdio>
+#include <cstdlib>
+#include <string>
+#include <vector>
 #include <cstdint>
 #include <vector>
 #include "../../paper_2407_21418_b200/csrc/ptx.cuh"
@@ -129,13 +132,27 @@ int main() {
   void* buf; cudaMalloc(&buf, K * R * 2); cudaMemset(buf, 0, K * R * 2);
   unsigned long long* out; cudaMalloc(&out, 148 * 8);
   const int ctas = 148, iters = 4000;
-  struct Cfg { int pair, N, S, mma, big = 0; } cfgs[] = {
+  struct Cfg { int pair, N, S, mma, big = 0; };
+  std::vector<Cfg> cfgs = {
       {0, 256, 4, 2}, {0, 256, 4, 7}, {0, 128, 4, 2}, {0, 128, 4, 7}, {0, 64, 4, 2}, {0, 64, 4, 7}, {0, 32, 4, 7},
       {0, 64, 8, 1, 1}, {0, 64, 8, 1, 0}, {0, 256, 4, 1, 1},
       {0, 64, 4, 5}, {0, 128, 4, 5}, {0, 256, 4, 5}, {0, 64, 4, 6}, {0, 128, 4, 6}, {1, 128, 4, 5}, {1, 64, 4, 5},
       {0, 128, 4, 2}, {0, 128, 4, 3}, {0, 128, 4, 4}, {0, 64, 4, 2}, {0, 64, 4, 3}, {0, 64, 4, 4}, {0, 32, 4, 4}, {1, 128, 4, 3}, {1, 64, 4, 4},
       {0, 256, 4, 1}, {0, 256, 4, 0}, {0, 128, 6, 1}, {0, 64, 8, 1}, {0, 256, 3, 1},
       {1, 256, 6, 1}, {1, 256, 6, 0}, {1, 256, 4, 1}, {1, 128, 8, 1}, {1, 64, 8, 1}};
+  if (const char* env = getenv("CFGS")) {  // "pair,N,S,mma,big;..."
+    cfgs.clear();
+    std::string all(env);
+    size_t p0 = 0;
+    while (p0 < all.size()) {
+      size_t p1 = all.find(';', p0);
+      if (p1 == std::string::npos) p1 = all.size();
+      Cfg c{};
+      sscanf(all.substr(p0, p1 - p0).c_str(), "%d,%d,%d,%d,%d", &c.pair, &c.N, &c.S, &c.mma, &c.big);
+      cfgs.push_back(c);
+      p0 = p1 + 1;
+    }
+  }
   int dbg = 0;
   for (auto& c : cfgs) {
     Maps m;
