@@ -141,7 +141,7 @@ struct TcConfig {
 constexpr int kTraceItems = 16;   // items traced per CTA
 constexpr int kTraceEvents = 6;   // see kernel_tc.cu
 constexpr int kTraceKb = 64;      // K blocks traced per CTA (producer issue, MMA sees data)
-constexpr int kTracePerCta = kTraceItems * kTraceEvents + 2 * kTraceKb;
+constexpr int kTracePerCta = kTraceItems * kTraceEvents + 2 * kTraceKb + 2;  // + CTA start / end stamps
 
 constexpr int kBlockK = 64;          // one 128-B swizzle atom of bf16 along K
 constexpr int kLaneRows = 128;       // MMA M

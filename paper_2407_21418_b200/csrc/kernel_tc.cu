@@ -211,6 +211,8 @@ __global__ void __launch_bounds__(kTcThreads, 1)
   // its wait, and every output write is causally after an operand load.
   // Dependents may launch right away — they in turn wait for this grid.
   griddep_launch_dependents();
+  if (threadIdx.x == 0 && cfg.trace)  // CTA start stamp
+    cfg.trace[static_cast<size_t>(blockIdx.x) * kTracePerCta + kTracePerCta - 2] = globaltimer();
   const int G = gridDim.x;
 
   if (warp == 0) {
@@ -464,6 +466,8 @@ __global__ void __launch_bounds__(kTcThreads, 1)
 
   tc_fence_before();
   __syncthreads();
+  if (threadIdx.x == 0 && cfg.trace)  // CTA end stamp (all epilogue stores issued and complete)
+    cfg.trace[static_cast<size_t>(blockIdx.x) * kTracePerCta + kTracePerCta - 1] = globaltimer();
   if (warp == 2) {
     tc_fence_after();
     tmem_dealloc<kTmemCols>(tmem_base);

@@ -195,7 +195,8 @@ class Executable:
 
     def read_trace(self):
         """(items [n_ctas, 16, 6], kblocks [n_ctas, 64, 2]) of %globaltimer ns
-        (0 = not reached); see include/ftb.h ftb_exec_set_trace."""
+        (0 = not reached); see include/ftb.h ftb_exec_set_trace. Also sets
+        ``self.trace_span`` = [n_ctas, 2] (CTA start, end stamps)."""
         import numpy as np
 
         L = _lib.lib()
@@ -203,9 +204,10 @@ class Executable:
         _lib.check(L.ftb_exec_read_trace(self._h, None, 0, C.byref(n)))
         out = np.zeros(n.value, dtype=np.uint64)
         _lib.check(L.ftb_exec_read_trace(self._h, out.ctypes.data_as(C.POINTER(C.c_uint64)), n.value, C.byref(n)))
-        per = 16 * 6 + 2 * 64
+        per = 16 * 6 + 2 * 64 + 2
         out = out.reshape(-1, per)
-        return out[:, : 16 * 6].reshape(-1, 16, 6), out[:, 16 * 6:].reshape(-1, 64, 2)
+        self.trace_span = out[:, -2:]  # per CTA: start, end stamps
+        return out[:, : 16 * 6].reshape(-1, 16, 6), out[:, 16 * 6: 16 * 6 + 128].reshape(-1, 64, 2)
 
     def table(self):
         """The lowered work items as an int32 numpy array [n_work, 8]."""
