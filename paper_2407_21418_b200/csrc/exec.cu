@@ -180,11 +180,16 @@ std::vector<Region> plan_regions(const ftb_gemm_desc& d, const ftb_program& g,
 struct Piece {
   int64_t start, len;
 };
-void split(int64_t lo, int64_t hi, int64_t maxlen, std::vector<Piece>& out) {
+// Cut [lo, hi) into n = ceil(len / maxlen) near-equal pieces whose lengths
+// are multiples of `align` (except the last). MN-major operands (B given as
+// [K, N]) need align = 8: TMA rejects an innermost box coordinate that is not
+// a multiple of 16 bytes (an unaligned piece start faults with an illegal
+// instruction, tests/test_fuzz_gpu.py); maxlen is a multiple of 8.
+void split(int64_t lo, int64_t hi, int64_t maxlen, std::vector<Piece>& out, int64_t align = 1) {
   out.clear();
   const int64_t len = hi - lo;
   const int64_t n = ceil_div(len, maxlen);
-  const int64_t base = ceil_div(len, n);
+  const int64_t base = std::min(maxlen, round_up(ceil_div(len, n), align));
   for (int64_t s = lo; s < hi; s += base) out.push_back({s, std::min(base, hi - s)});
 }
 
@@ -367,12 +372,15 @@ static void build(ExecImpl& ex, const ftb_gemm_desc* probs, const ftb_program* p
       const int64_t b0 = ib ? r.lo[0] : 0, b1 = ib ? r.hi[0] : 1;
       const int64_t ilo = r.lo[ib], ihi = r.hi[ib], jlo = r.lo[ib + 1], jhi = r.hi[ib + 1];
       if (swap) {
-        split(jlo, jhi, lane_max, lp);
-        split(ilo, ihi, col_max, cp);
+        split(jlo, jhi, lane_max, lp, P.lane_mn ? 8 : 1);
+        split(ilo, ihi, col_max, cp, P.col_mn ? 8 : 1);
       } else {
-        split(ilo, ihi, lane_max, lp);
-        split(jlo, jhi, col_max, cp);
+        split(ilo, ihi, lane_max, lp, P.lane_mn ? 8 : 1);
+        split(jlo, jhi, col_max, cp, P.col_mn ? 8 : 1);
       }
+      if ((P.lane_mn && lp.front().start % 8) || (P.col_mn && cp.front().start % 8))
+        throw input_error("B given as [K, N] needs uKernel tiles along N that start on multiples of 8 "
+                          "(TMA 16-byte box origin); pass B as [N, K] (b_layout nk)", "smem_tile");
       for (int64_t b = b0; b < b1; ++b)
         for (auto& L : lp)
           for (auto& Cc : cp) {

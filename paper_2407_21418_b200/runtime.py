@@ -67,8 +67,44 @@ class PlanRecord:
                 "fallback_stage": self.stage, "tuning_s": self.tuning_s, "counts": self.counts}
 
 
+def native_cover_program(inst: WorkloadInstance) -> _lib.Program:
+    """Last rung of the runtime planner's fallback ladder (beyond the
+    reference): an exact cover of the composition axis built directly from
+    executor tiles, for shapes whose uKernel candidates admit no exact
+    combination (e.g. a main-axis extent that is not a multiple of the
+    64-element alignment; the reference raises EmptyResultError there,
+    combine.py:183-188, and so does the mktune facade). BMM: tau = batch, one
+    entry per tile. Dense: tau = i, 128-row tiles plus one ragged tile. Other
+    space axes: uniform tiles (the executor cuts every rectangle into MMA
+    items anyway); reduce tile 64; register tiles 1."""
+    from .execute import program_struct
+
+    spec = inst.spec
+    space = list(spec.space_axes)
+    ext = inst.extents
+    if len(space) == 3:  # BMM: b, i, j
+        tau = 0
+        tiles = [1, min(ext[space[1]], 128), min(ext[space[2]], 256), 64]
+        parts = [([1, 1, 1], tiles, ext[space[0]])]
+    else:  # Dense: i, j
+        tau = 0
+        M = ext[space[0]]
+        jt = min(ext[space[1]], 256)
+        full, rem = divmod(M, 128)
+        parts = []
+        if full:
+            parts.append(([1, 1], [128, jt, 64], full))
+        if rem:
+            parts.append(([1, 1], [rem, jt, 64], 1))
+    return program_struct(len(space), tau, parts)
+
+
 class Planner:
-    """Thread-safe plan cache over the C++ planner."""
+    """Thread-safe plan cache over the C++ planner. Shapes whose candidates
+    admit no exact cover even after the C++ fallback ladder get
+    `native_cover_program` (relaxation "native-cover", stage -1) unless
+    ``native_cover`` is False (or FTB_NATIVE_COVER=0), in which case the
+    reference's EmptyResultError is raised."""
 
     def __init__(self, hw: HardwareDescriptor | None = None, params: FilterParams | None = None,
                  coeffs: SiaCoeffs | None = None, threads: int = 0):
@@ -78,6 +114,7 @@ class Planner:
             coeffs = SiaCoeffs(*(float(v) for v in os.environ["FTB_SIA_COEFFS"].split(",")))
         self.coeffs = coeffs or SiaCoeffs()
         self.threads = threads
+        self.native_cover = os.environ.get("FTB_NATIVE_COVER", "1") != "0"
         self._cache: dict[tuple, PlanRecord] = {}
         self._exe_cache: dict[tuple, Executable] = {}  # insertion-ordered LRU of lowered tables
         self.exe_cache_size = 32
@@ -107,6 +144,12 @@ class Planner:
                 C.byref(_native.hw_struct(self.hw)), insts, n, C.byref(_native.params_struct(self.params)),
                 C.byref(_native.coeffs_struct(self.coeffs)), self.threads, progs, reps, stats))
             for q, j in enumerate(todo):
+                if stats[q] == _lib.FTB_EMPTY_RESULT and self.native_cover:
+                    rec = PlanRecord(program=native_cover_program(instances[j]), tuning_s=reps[q].seconds,
+                                     relaxation="native-cover", stage=-1, counts={})
+                    with self._lock:
+                        self._cache[keys[j]] = rec
+                    continue
                 if stats[q] != 0:
                     # re-plan alone to surface the exact error text / class
                     one = (_native.Inst * 1)(insts[q])

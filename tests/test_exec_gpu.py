@@ -212,3 +212,26 @@ def test_column_split_and_split_k_lowerings(cuda, monkeypatch, M, N, K):
         ex.close()
     assert torch.equal(outs[("0", "0")], outs[("1", "0")])
     assert _rel(outs[("1", "1")], ref) < BF16_TOL
+
+
+@pytest.mark.parametrize("T", [200, 228, 300])
+def test_bmm_kn_layout_split_pieces_tma_aligned(cuda, T):
+    """B given as [K, N] makes the column (or, swapped, the lane) operand
+    MN-major; the executor's pieces of a > 128-lane / > 256-column rectangle
+    must start on multiples of 8 elements (TMA 16-byte box origin). A balanced
+    split at 114 or 100 used to fault with an illegal instruction (found by
+    tests/test_fuzz_gpu.py)."""
+    from paper_2407_21418_b200.runtime import Planner, bmm_instance
+
+    g = torch.Generator(device="cpu").manual_seed(T)
+    pad = (T + 7) // 8 * 8
+    A = (torch.rand(1, T, 64, generator=g) * 2 - 1).bfloat16().to(cuda)
+    B = (torch.rand(1, 64, pad, generator=g) * 2 - 1).bfloat16().to(cuda)[:, :, :T]
+    Cb = torch.full((1, T, pad), float("nan"), dtype=torch.bfloat16, device=cuda)
+    C = Cb[:, :, :T]
+    rec = Planner().plan([bmm_instance(1, T, T, 64)])[0]
+    ex = Executable([gemm_desc(A, B, C, "kn")], [rec.program], (A, B, Cb))
+    ex.launch()
+    torch.cuda.synchronize()
+    assert _rel(C, A.double() @ B.double()) < BF16_TOL
+    assert torch.isnan(Cb[:, :, T:].float()).all()

@@ -75,3 +75,18 @@ def test_padding_ratio_matches_covered_extents():
     d = desc(_lib.OP_DENSE, 1, 53, 768, 768)
     _, info = lower_table([d], [program_struct(2, 1, [((1, 8), (8, 64, 64), 12)])])
     assert info.covered_out == 56 * 768 and info.true_out == 53 * 768
+
+
+@pytest.mark.parametrize("T", [129, 200, 228, 300, 520])
+@pytest.mark.parametrize("orientation", [0, 1])
+def test_mn_major_piece_starts_are_tma_aligned(T, orientation):
+    """B as [K, N] (MN-major column/lane operand): every piece along N starts
+    on a multiple of 8 elements (16-byte TMA box origin) and the pieces still
+    tile C exactly once."""
+    d = desc(_lib.OP_BMM, 1, T, T, 64, b_layout=_lib.B_KN, orientation=orientation)
+    t, _ = lower_table([d], [program_struct(3, 1, [((1, 1, 1), (1, T, 64 * ((T + 63) // 64), 64), 1)])])
+    swap = orientation == 1
+    for _, b, l0, c0, ll, cl, nm, _ in t:
+        n_start = l0 if swap else c0
+        assert n_start % 8 == 0
+    assert (apply(t, d, swap) == 1).all()
