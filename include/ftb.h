@@ -224,7 +224,7 @@ void ftb_exec_destroy(ftb_exec* ex);
  * items of every CTA on subsequent launches; read back per CTA as
  * [16 items][6 events] (producer pick, K0 issued, K0 landed, MMA commit,
  * epilogue start, epilogue release), [64 K blocks][2] (producer issued, MMA
- * saw data), then the CTA's start and end stamps. */
+ * saw data), then the CTA's start and end stamps (builds with FTB_TRACE_SPAN). */
 ftb_status ftb_exec_set_trace(ftb_exec* ex, int32_t enable);
 ftb_status ftb_exec_read_trace(const ftb_exec* ex, uint64_t* out, int64_t cap, int64_t* n_out);
 /* Pipeline shapes chosen for the table, 10 ints: single-CTA kernel {stages,

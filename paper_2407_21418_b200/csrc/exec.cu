@@ -371,12 +371,15 @@ static void build(ExecImpl& ex, const ftb_gemm_desc* probs, const ftb_program* p
     for (const Region& r : regs) {
       const int64_t b0 = ib ? r.lo[0] : 0, b1 = ib ? r.hi[0] : 1;
       const int64_t ilo = r.lo[ib], ihi = r.hi[ib], jlo = r.lo[ib + 1], jhi = r.hi[ib + 1];
+      // j is C's innermost dimension (and B's when B is [K, N]): pieces along
+      // j start on multiples of 8 elements so TMA store (and MN-major load)
+      // boxes have 16-byte origins
       if (swap) {
-        split(jlo, jhi, lane_max, lp, P.lane_mn ? 8 : 1);
-        split(ilo, ihi, col_max, cp, P.col_mn ? 8 : 1);
+        split(jlo, jhi, lane_max, lp, 8);
+        split(ilo, ihi, col_max, cp, 1);
       } else {
-        split(ilo, ihi, lane_max, lp, P.lane_mn ? 8 : 1);
-        split(jlo, jhi, col_max, cp, P.col_mn ? 8 : 1);
+        split(ilo, ihi, lane_max, lp, 1);
+        split(jlo, jhi, col_max, cp, 8);
       }
       if ((P.lane_mn && lp.front().start % 8) || (P.col_mn && cp.front().start % 8))
         throw input_error("B given as [K, N] needs uKernel tiles along N that start on multiples of 8 "
@@ -445,7 +448,10 @@ static void upload(ExecImpl& I) {
   auto tma_ok = [&](const DevWork& w) {
     const DevProblem& P = I.problems[w.problem];
     const int32_t lane_ext = P.swap ? P.N : P.M, col_ext = P.swap ? P.M : P.N;
-    return tma_store_on && I.tma_out[w.problem] && (w.lane_len % 32 == 0 || w.lane0 + w.lane_len == lane_ext) &&
+    // ... and the box origin along C's innermost dimension (j) is 16-byte aligned
+    const int32_t j0 = P.swap ? w.lane0 : w.col0;
+    return tma_store_on && I.tma_out[w.problem] && j0 % 8 == 0 &&
+           (w.lane_len % 32 == 0 || w.lane0 + w.lane_len == lane_ext) &&
            (w.col_len % 32 == 0 || w.col0 + w.col_len == col_ext);
   };
   // CTA pairs: logical items of one problem/batch with the same column range

@@ -211,8 +211,13 @@ __global__ void __launch_bounds__(kTcThreads, 1)
   // its wait, and every output write is causally after an operand load.
   // Dependents may launch right away — they in turn wait for this grid.
   griddep_launch_dependents();
-  if (threadIdx.x == 0 && cfg.trace)  // CTA start stamp
+#ifdef FTB_TRACE_SPAN
+  // CTA start / end stamps (scripts/tail_spread.py). Debug builds only: these
+  // two guarded stores alone cost the release kernel ~13 % on the C1 step
+  // (register allocation / scheduling of the whole kernel changes).
+  if (threadIdx.x == 0 && cfg.trace)
     cfg.trace[static_cast<size_t>(blockIdx.x) * kTracePerCta + kTracePerCta - 2] = globaltimer();
+#endif
   const int G = gridDim.x;
 
   if (warp == 0) {
@@ -466,8 +471,10 @@ __global__ void __launch_bounds__(kTcThreads, 1)
 
   tc_fence_before();
   __syncthreads();
+#ifdef FTB_TRACE_SPAN
   if (threadIdx.x == 0 && cfg.trace)  // CTA end stamp (all epilogue stores issued and complete)
     cfg.trace[static_cast<size_t>(blockIdx.x) * kTracePerCta + kTracePerCta - 1] = globaltimer();
+#endif
   if (warp == 2) {
     tc_fence_after();
     tmem_dealloc<kTmemCols>(tmem_base);

@@ -2,7 +2,9 @@
 its first item and when its last epilogue retires (device globaltimer, the
 trace's item events; the last traced item of a CTA may not be its last item,
 so the end is read from a dedicated per-CTA end stamp: the maximum of all
-release events). Reports the spread of CTA end times."""
+release events). Reports the spread of CTA end times. Needs a build with -DFTB_TRACE_SPAN
+(the stamps are compiled out of the release kernel):
+  make -C paper_2407_21418_b200/csrc BUILD=/tmp/vbs NVFLAGS="... -DFTB_TRACE_SPAN"."""
 import sys
 sys.path.insert(0, ".")
 import numpy as np, torch

@@ -235,3 +235,22 @@ def test_bmm_kn_layout_split_pieces_tma_aligned(cuda, T):
     torch.cuda.synchronize()
     assert _rel(C, A.double() @ B.double()) < BF16_TOL
     assert torch.isnan(Cb[:, :, T:].float()).all()
+
+
+@pytest.mark.parametrize("M", [129, 130, 160])
+def test_dense_swap_tma_store_origin_aligned(cuda, M):
+    """Swap-AB puts output columns on the lanes: a 232-column rectangle used
+    to be cut 116 + 116, giving a TMA store box origin at column 884 (not
+    16-byte aligned): illegal instruction (found by tests/test_fuzz_gpu.py)."""
+    from paper_2407_21418_b200.runtime import Planner, dense_instance
+
+    N, K = 1000, 256
+    A, B, ref = _dense(M, N, K, "nk", torch.bfloat16, cuda, seed=M)
+    Cb = torch.full((M, 1008), float("nan"), dtype=torch.bfloat16, device=cuda)
+    C = Cb[:, :N]
+    rec = Planner().plan([dense_instance(M, N, K)])[0]
+    ex = Executable([gemm_desc(A, B, C, "nk", orientation=1)], [rec.program], (A, B, Cb))
+    ex.launch()
+    torch.cuda.synchronize()
+    assert _rel(C, ref) < BF16_TOL
+    assert torch.isnan(Cb[:, N:].float()).all()

@@ -111,3 +111,51 @@ def test_random_problems_alone_and_grouped(cuda, seed):
     for p in probs:
         _check(p, "grouped")
     ex.close()
+
+
+@pytest.mark.parametrize("mode", ["FTB_TMA_STORE=0", "FTB_SPLITK=0", "FTB_COLSPLIT=0", "FTB_PAIR=1", "FTB_NO_PACK=1"])
+@pytest.mark.parametrize("orientation", [0, 1])
+def test_random_problems_forced_orientation_and_modes(cuda, monkeypatch, mode, orientation):
+    """The same sweep with the orientation forced (0 normal, 1 swap-AB) and
+    one executor switch flipped, one grouped table per case."""
+    k, v = mode.split("=")
+    monkeypatch.setenv(k, v)
+    seed = 100 + 10 * orientation + len(mode)
+    rng = random.Random(seed)
+    g = torch.Generator(device="cpu").manual_seed(seed)
+    probs = [_draw(rng, g, cuda) for _ in range(24)]
+    recs = Planner().plan([p["inst"] for p in probs])
+    descs = [gemm_desc(p["A"], p["B"], p["C"], p["b_layout"], orientation=orientation, bias=p["bias"],
+                       activation=p["act"]) for p in probs]
+    ex = Executable(descs, [r.program for r in recs], [t for p in probs for t in p["keep"]])
+    ex.launch()
+    torch.cuda.synchronize()
+    for p in probs:
+        _check(p, f"{mode} orientation={orientation}")
+    ex.close()
+
+
+@pytest.mark.parametrize("seed", [7, 8])
+def test_random_fp32_ffma_problems(cuda, seed):
+    """fp32 validation mode (config C0 family): random Dense extents and
+    layouts on the FFMA kernel, 1e-5 against float64."""
+    from paper_2407_21418_b200.runtime import dense_instance
+
+    rng = random.Random(seed)
+    g = torch.Generator(device="cpu").manual_seed(seed)
+    planner = Planner(hw=__import__("paper_2407_21418_b200.mktune.hardware", fromlist=["b200_ffma"]).b200_ffma())
+    for _ in range(12):
+        M, N, K = rng.randint(1, 600), rng.choice([1, 33, 64, 100, 768]), rng.choice([1, 7, 64, 300, 768])
+        b_layout = rng.choice(["kn", "nk"])
+        A_base, A = _padded((M, K), torch.float32, cuda, g)
+        B_base, B = _padded((K, N) if b_layout == "kn" else (N, K), torch.float32, cuda, g)
+        C_base, C = _padded((M, N), torch.float32, cuda, g, fill=float("nan"))
+        rec = planner.plan([dense_instance(M, N, K, elem_bytes=4, m_max=512)])[0]
+        ex = Executable([gemm_desc(A, B, C, b_layout)], [rec.program], (A_base, B_base, C_base))
+        ex.launch()
+        torch.cuda.synchronize()
+        ref = A.double() @ (B.double() if b_layout == "kn" else B.double().t())
+        err = ((C.double() - ref).abs().max() / ref.abs().max().clamp_min(1e-30)).item()
+        assert err < 1e-5, (M, N, K, b_layout, err)
+        assert torch.isnan(C_base[:, N:]).all()
+        ex.close()

@@ -90,3 +90,17 @@ def test_mn_major_piece_starts_are_tma_aligned(T, orientation):
         n_start = l0 if swap else c0
         assert n_start % 8 == 0
     assert (apply(t, d, swap) == 1).all()
+
+
+@pytest.mark.parametrize("b_layout", [_lib.B_NK, _lib.B_KN])
+@pytest.mark.parametrize("orientation", [0, 1])
+@pytest.mark.parametrize("N", [232, 300, 1000])
+def test_output_column_piece_starts_are_tma_aligned(b_layout, orientation, N):
+    """Pieces along j (C's innermost dimension) start on multiples of 8 in
+    both orientations: TMA store boxes need 16-byte origins."""
+    d = desc(_lib.OP_DENSE, 1, 130, N, 256, b_layout=b_layout, orientation=orientation)
+    t, _ = lower_table([d], [program_struct(2, 0, [((1, 1), (130, 256, 64), 1)])])
+    swap = orientation == 1
+    for _, b, l0, c0, ll, cl, nm, _ in t:
+        assert (l0 if swap else c0) % 8 == 0
+    assert (apply(t, d, swap) == 1).all()
