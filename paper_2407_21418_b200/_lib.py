@@ -14,6 +14,11 @@ from pathlib import Path
 
 _HERE = Path(__file__).resolve().parent
 LIB_PATH = _HERE / "libftb.so"
+# FTB_LIB: load another build of the library, e.g. the trace build
+# (make -C paper_2407_21418_b200/csrc trace -> libftb_trace.so) for the
+# phase-trace scripts under scripts/.
+if os.environ.get("FTB_LIB"):
+    LIB_PATH = Path(os.environ["FTB_LIB"]).resolve()
 
 MAX_AXES = 8
 

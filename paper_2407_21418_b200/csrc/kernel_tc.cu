@@ -44,11 +44,17 @@ __device__ __forceinline__ TcWork load_work(const TcWork* __restrict__ work, int
 //   2 MMA saw K block 0 land        3 MMA committed the item
 //   4 epilogue saw the accumulator  5 epilogue released it
 __device__ __forceinline__ void trace_ev(const TcConfig& cfg, uint32_t local, int ev) {
+#ifndef FTB_TRACE
+  return;  // release build: phase tracing compiled out (it costs ~6 % per launch)
+#endif
   if (cfg.trace && local < kTraceItems)
     cfg.trace[static_cast<size_t>(blockIdx.x) * kTracePerCta + local * kTraceEvents + ev] = globaltimer();
 }
 // per-K-block events of the first kTraceKb K blocks: 0 producer issued, 1 MMA saw data
 __device__ __forceinline__ void trace_kb(const TcConfig& cfg, uint32_t g, int ev) {
+#ifndef FTB_TRACE
+  return;
+#endif
   if (cfg.trace && g < kTraceKb)
     cfg.trace[static_cast<size_t>(blockIdx.x) * kTracePerCta + kTraceItems * kTraceEvents + 2 * g + ev] =
         globaltimer();
@@ -211,7 +217,7 @@ __global__ void __launch_bounds__(kTcThreads, 1)
   // its wait, and every output write is causally after an operand load.
   // Dependents may launch right away — they in turn wait for this grid.
   griddep_launch_dependents();
-#ifdef FTB_TRACE_SPAN
+#ifdef FTB_TRACE
   // CTA start / end stamps (scripts/tail_spread.py). Debug builds only: these
   // two guarded stores alone cost the release kernel ~13 % on the C1 step
   // (register allocation / scheduling of the whole kernel changes).
@@ -471,7 +477,7 @@ __global__ void __launch_bounds__(kTcThreads, 1)
 
   tc_fence_before();
   __syncthreads();
-#ifdef FTB_TRACE_SPAN
+#ifdef FTB_TRACE
   if (threadIdx.x == 0 && cfg.trace)  // CTA end stamp (all epilogue stores issued and complete)
     cfg.trace[static_cast<size_t>(blockIdx.x) * kTracePerCta + kTracePerCta - 1] = globaltimer();
 #endif

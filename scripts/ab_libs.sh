@@ -2,7 +2,8 @@
 # (each copied over paper_2407_21418_b200/libftb.so in turn; step + per-shape mean)
 orig=$(mktemp); cp paper_2407_21418_b200/libftb.so $orig
 for r in 1 2; do for L in "$@"; do
-  cp $L paper_2407_21418_b200/libftb.so
+  src=$L; [ "$(realpath $L)" = "$(realpath paper_2407_21418_b200/libftb.so)" ] && src=$orig  # the live lib: its saved copy
+  cp $src paper_2407_21418_b200/libftb.so
   timeout 300 python bench.py --steps 30 --warmup 5 --no-cpu --per-shape-rows --min-warm-s 0.5 2>&1 | tail -1 | python -c "
 import json,sys,collections
 d=json.loads(sys.stdin.read()); g=collections.defaultdict(list)

@@ -2,6 +2,8 @@
 items in the grouped C1 step: a cold instruction cache shows up as a slow
 first epilogue."""
 import os, sys
+import os as _os
+_os.environ.setdefault("FTB_LIB", "paper_2407_21418_b200/libftb_trace.so")  # phase traces need the trace build (make -C paper_2407_21418_b200/csrc trace)
 sys.path.insert(0, ".")
 import numpy as np, torch
 from paper_2407_21418_b200.runtime import Planner

@@ -2,6 +2,8 @@
 SHAPE="M N K" (Dense, nk); prints CUDA-event time per launch vs the device
 trace span (first producer pick -> last epilogue release) per CTA."""
 import os, sys
+import os as _os
+_os.environ.setdefault("FTB_LIB", "paper_2407_21418_b200/libftb_trace.so")  # phase traces need the trace build (make -C paper_2407_21418_b200/csrc trace)
 sys.path.insert(0, ".")
 import numpy as np, torch
 from paper_2407_21418_b200.execute import Executable, gemm_desc

@@ -2,6 +2,8 @@
 gap = (first K block of item i lands) - (item i-1 committed), i.e. time the
 MMA warp waited for data. BMM (1-2 K blocks: MMA span < 1 us) vs Dense (>= 12 K blocks)."""
 import sys
+import os as _os
+_os.environ.setdefault("FTB_LIB", "paper_2407_21418_b200/libftb_trace.so")  # phase traces need the trace build (make -C paper_2407_21418_b200/csrc trace)
 sys.path.insert(0, ".")
 import numpy as np, torch
 from paper_2407_21418_b200.runtime import Planner

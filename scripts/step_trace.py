@@ -1,5 +1,7 @@
 """Phase trace of the C1 step table (first 16 items of every CTA)."""
 import os, sys
+import os as _os
+_os.environ.setdefault("FTB_LIB", "paper_2407_21418_b200/libftb_trace.so")  # phase traces need the trace build (make -C paper_2407_21418_b200/csrc trace)
 sys.path.insert(0, ".")
 import numpy as np, torch
 from paper_2407_21418_b200.runtime import Planner

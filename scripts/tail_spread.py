@@ -2,10 +2,12 @@
 its first item and when its last epilogue retires (device globaltimer, the
 trace's item events; the last traced item of a CTA may not be its last item,
 so the end is read from a dedicated per-CTA end stamp: the maximum of all
-release events). Reports the spread of CTA end times. Needs a build with -DFTB_TRACE_SPAN
+release events). Reports the spread of CTA end times. Needs the trace build
 (the stamps are compiled out of the release kernel):
-  make -C paper_2407_21418_b200/csrc BUILD=/tmp/vbs NVFLAGS="... -DFTB_TRACE_SPAN"."""
+  make -C paper_2407_21418_b200/csrc trace (libftb_trace.so)."""
 import sys
+import os as _os
+_os.environ.setdefault("FTB_LIB", "paper_2407_21418_b200/libftb_trace.so")  # phase traces need the trace build (make -C paper_2407_21418_b200/csrc trace)
 sys.path.insert(0, ".")
 import numpy as np, torch
 from paper_2407_21418_b200.runtime import Planner

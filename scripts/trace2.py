@@ -1,4 +1,6 @@
 import os, sys
+import os as _os
+_os.environ.setdefault("FTB_LIB", "paper_2407_21418_b200/libftb_trace.so")  # phase traces need the trace build (make -C paper_2407_21418_b200/csrc trace)
 os.environ.setdefault("FTB_PAIR", "0")
 sys.path.insert(0, ".")
 import numpy as np, torch
