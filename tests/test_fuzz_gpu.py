@@ -159,3 +159,67 @@ def test_random_fp32_ffma_problems(cuda, seed):
         assert err < 1e-5, (M, N, K, b_layout, err)
         assert torch.isnan(C_base[:, N:]).all()
         ex.close()
+
+
+def _draw_large(rng, g, dev):
+    """Bigger extents: Dense M up to 8192 with K up to 4096 (split-K for the
+    small-table cases, fused bias/GELU, fp32 outputs), BMM batch up to 1024
+    with T up to 512 (C2's range), both layouts."""
+    if rng.random() < 0.5:
+        M = int(math.exp(rng.uniform(0.0, math.log(8192.0))))
+        N = rng.choice([128, 768, 1000, 2304, 3072, 4096])
+        K = rng.choice([768, 1000, 3072, 4096])
+        b_layout = rng.choice(["kn", "nk"])
+        out_dtype = torch.float32 if rng.random() < 0.2 else torch.bfloat16
+        A_base, A = _padded((M, K), torch.bfloat16, dev, g)
+        B_base, B = _padded((K, N) if b_layout == "kn" else (N, K), torch.bfloat16, dev, g)
+        C_base, C = _padded((M, N), out_dtype, dev, g, fill=float("nan"))
+        bias = act = None
+        if rng.random() < 0.4:
+            bias = ((torch.rand(N, generator=g) * 2 - 1) * 0.5).to(torch.bfloat16).to(dev)
+            act = "gelu" if rng.random() < 0.5 else None
+        Bkn = B.double() if b_layout == "kn" else B.double().t()
+        ref = A.double() @ Bkn
+        if bias is not None:
+            ref = ref + bias.double()
+        if act == "gelu":
+            ref = F.gelu(ref)
+        return dict(inst=dense_instance(M, N, K), A=A, B=B, C=C, C_base=C_base, b_layout=b_layout, bias=bias,
+                    act=act, ref=ref, keep=(A_base, B_base, C_base),
+                    name=f"dense M{M} N{N} K{K} {b_layout} {out_dtype} bias={bias is not None} {act}")
+    b = rng.choice([64, 384, 1024])
+    T = rng.randint(1, 512)
+    kind = rng.choice(["scores", "context"])
+    M, N, K, dyn, b_layout = (T, T, 64, ("i", "j"), "nk") if kind == "scores" else (T, 64, T, ("i", "k"), "kn")
+    out_dtype = torch.float32 if rng.random() < 0.15 else torch.bfloat16
+    A_base, A = _padded((b, M, K), torch.bfloat16, dev, g)
+    B_base, B = _padded((b, K, N) if b_layout == "kn" else (b, N, K), torch.bfloat16, dev, g)
+    C_base, C = _padded((b, M, N), out_dtype, dev, g, fill=float("nan"))
+    Bkn = B.double() if b_layout == "kn" else B.double().transpose(1, 2)
+    return dict(inst=bmm_instance(b, M, N, K, dyn), A=A, B=B, C=C, C_base=C_base, b_layout=b_layout, bias=None,
+                act=None, ref=A.double() @ Bkn, keep=(A_base, B_base, C_base),
+                name=f"bmm {kind} b{b} T{T} {b_layout} {out_dtype}")
+
+
+@pytest.mark.parametrize("seed", [21, 22, 23])
+def test_random_large_problems_alone_and_grouped(cuda, seed):
+    rng = random.Random(seed)
+    g = torch.Generator(device="cpu").manual_seed(seed)
+    probs = [_draw_large(rng, g, cuda) for _ in range(8)]
+    recs = Planner().plan([p["inst"] for p in probs])
+    for p, r in zip(probs, recs):
+        ex = Executable([gemm_desc(p["A"], p["B"], p["C"], p["b_layout"], bias=p["bias"], activation=p["act"])],
+                        [r.program], p["keep"])
+        ex.launch()
+        torch.cuda.synchronize()
+        _check(p, "alone")
+        ex.close()
+    for p in probs:
+        p["C_base"].fill_(float("nan"))
+    descs = [gemm_desc(p["A"], p["B"], p["C"], p["b_layout"], bias=p["bias"], activation=p["act"]) for p in probs]
+    ex = Executable(descs, [r.program for r in recs], [t for p in probs for t in p["keep"]])
+    ex.launch()
+    torch.cuda.synchronize()
+    for p in probs:
+        _check(p, "grouped")
+    ex.close()
