@@ -37,10 +37,16 @@ __device__ __forceinline__ TcPair load_pair(const TcPair* __restrict__ work, int
 }
 
 __device__ __forceinline__ void trace2_ev(const TcConfig& cfg, uint32_t local, int ev) {
+#ifndef FTB_TRACE
+  return;  // release build: tracing compiled out (see kernel_tc.cu)
+#endif
   if (cfg.trace && local < kTraceItems)
     cfg.trace[static_cast<size_t>(blockIdx.x) * kTracePerCta + local * kTraceEvents + ev] = globaltimer();
 }
 __device__ __forceinline__ void trace2_kb(const TcConfig& cfg, uint32_t g, int ev) {
+#ifndef FTB_TRACE
+  return;
+#endif
   if (cfg.trace && g < kTraceKb)
     cfg.trace[static_cast<size_t>(blockIdx.x) * kTracePerCta + kTraceItems * kTraceEvents + 2 * g + ev] =
         globaltimer();
