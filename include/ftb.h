@@ -214,7 +214,10 @@ typedef struct {
  * describes; the table is validated against that before upload. */
 ftb_status ftb_exec_create(const ftb_gemm_desc* problems, const ftb_program* programs,
                            int32_t n, ftb_exec** out);
-/* Launch the table as one persistent kernel on `stream` (cudaStream_t). */
+/* Launch the table as one persistent kernel on `stream` (cudaStream_t).
+ * Launches of one executable must be stream-ordered (not concurrent on two
+ * streams): a split-K table keeps its fp32 partials and arrival counters in
+ * per-executable device memory. */
 ftb_status ftb_exec_launch(ftb_exec* ex, void* stream);
 ftb_status ftb_exec_get_info(const ftb_exec* ex, ftb_exec_info* info);
 /* Host copy of the lowered table (int32 x 8 per work item), for tests. */

@@ -46,6 +46,9 @@ def time_launches(launch, reps: int = 10, rounds: int = 3) -> float:
     """Microseconds per launch: `reps` launches captured in a CUDA graph, best of `rounds`."""
     import torch
 
+    # launches of one table must not overlap each other (the split-K workspace
+    # and its counters are per table): drain earlier work on other streams first
+    torch.cuda.synchronize()
     s = torch.cuda.Stream()
     with torch.cuda.stream(s):
         launch(s)

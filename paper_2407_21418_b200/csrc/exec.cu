@@ -605,6 +605,34 @@ static void upload(ExecImpl& I) {
     const bool split_wide = env_w && env_w[0] == '1';
     if (split_on && n_items > 0 && n_items * 2 <= sms_here) {
       const int target = static_cast<int>(std::min<int64_t>(kMaxSplit, sms_here / n_items));
+      // On-chip mode: when every item can be split the same way (s = 4 or 2,
+      // >= split_min_kb K blocks per split) and the whole table fits the
+      // co-resident clusters (measured: 33 clusters of 4, 74 of 2 at ~200 KiB
+      // smem per CTA, scripts/micro/cluster_occ.cu), the splits of a tile
+      // become one cluster and reduce through distributed shared memory
+      // (kernel_tc.cu cluster_reduce) — no fp32 workspace round trip.
+      const char* env_cl = std::getenv("FTB_SPLIT_CLUSTER");
+      const bool cluster_on = !(env_cl && env_cl[0] == '0');
+      int s_cl = 0;
+      if (cluster_on) {
+        int s_glob = 0;  // the global-workspace path's split count
+        for (const TcWork& t : tw)
+          if (!t.pack && (t.n_mma <= 128 || split_wide)) s_glob = std::max(s_glob, std::min(target, t.num_kb / split_min_kb));
+        for (int cand : {4, 2}) {
+          if (cand > target) continue;
+          bool ok = true;
+          for (const TcWork& t : tw) ok = ok && !t.pack && t.n_mma <= 128 && t.num_kb / split_min_kb >= cand;
+          const int64_t cap = std::min<int64_t>(cand == 4 ? 132 : 148, sms_here);
+          if (ok && n_items * cand <= cap) {
+            s_cl = cand;
+            break;
+          }
+        }
+        // on chip unless it gives up more than a third of the splits the
+        // workspace path would use (measured: C1 FFN2 M=768, 2 vs 4 splits:
+        // 13.0 vs 11.6 us; M=1024, 2 vs 3: 13.8 vs 14.3 us)
+        if (s_cl && 3 * s_cl < 2 * s_glob) s_cl = 0;
+      }
       std::vector<TcWork> split;
       int32_t tiles = 0;
       for (const TcWork& t : tw) {
@@ -612,7 +640,7 @@ static void upload(ExecImpl& I) {
         // round trip (128 x n_mma x 8 B) must stay small next to the operand
         // bytes a split saves (measured: C3 M<=127 22 -> 18 us, M=256 n=256
         // tiles 23 -> 28 us when split)
-        const int s_t = (t.n_mma <= 128 || split_wide) ? std::min(target, t.num_kb / split_min_kb) : 1;
+        const int s_t = s_cl ? s_cl : ((t.n_mma <= 128 || split_wide) ? std::min(target, t.num_kb / split_min_kb) : 1);
         if (t.pack || s_t < 2) {
           split.push_back(t);
           continue;
@@ -632,7 +660,10 @@ static void upload(ExecImpl& I) {
       }
       // the split epilogue's all-splits rendezvous needs every item resident
       // at once: one item per CTA, at most one CTA per SM
-      if (tiles > 0 && static_cast<int64_t>(split.size()) <= sms_here) {
+      if (tiles > 0 && s_cl) {
+        I.cfg.cluster_split = s_cl;  // partials stay on chip: no workspace
+        tw.swap(split);
+      } else if (tiles > 0 && static_cast<int64_t>(split.size()) <= sms_here) {
         FTB_CUDA(cudaMalloc(&I.d_split_ws, sizeof(float) * static_cast<size_t>(tiles) * kSplitTileFloats));
         FTB_CUDA(cudaMalloc(&I.d_split_cnt, sizeof(int32_t) * 8 * tiles));
         FTB_CUDA(cudaMemset(I.d_split_cnt, 0, sizeof(int32_t) * 8 * tiles));
@@ -651,7 +682,7 @@ static void upload(ExecImpl& I) {
     auto cost = [](const TcWork& t) { return static_cast<int64_t>(t.num_kb) * std::max(kMmaFloorN, t.n_mma); };
     std::vector<TcWork> lng, shrt;
     for (const TcWork& t : tw) (cost(t) >= 4 * kMmaFloorN ? lng : shrt).push_back(t);
-    if (!(env_il && env_il[0] == '0') && !lng.empty() && !shrt.empty()) {
+    if (!(env_il && env_il[0] == '0') && I.cfg.cluster_split <= 1 && !lng.empty() && !shrt.empty()) {
       std::vector<TcWork> mix;
       mix.reserve(tw.size());
       size_t a = 0, b = 0;

@@ -137,6 +137,8 @@ struct TcConfig {
   unsigned long long* trace;  // optional: per-CTA phase timestamps (debug)
   float* split_ws;            // split-K partials [tile][split][128][256] fp32
   int32_t* split_cnt;         // split-K counters [tile][arrive, depart][4 lane quadrants]
+  int32_t cluster_split;      // > 1: split-K partials reduced on chip across a cluster of this many CTAs
+  int32_t pad_;
 };
 constexpr int kTraceItems = 16;   // items traced per CTA
 constexpr int kTraceEvents = 6;   // see kernel_tc.cu

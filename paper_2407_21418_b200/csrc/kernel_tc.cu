@@ -81,11 +81,27 @@ __device__ __forceinline__ TcWork bcast_work(uint32_t mine) {
 // splits for this quadrant sums all partials (fixed split order, so the sum is
 // deterministic) and stores C through the predicated path, then re-arms the
 // counter for the next launch.
-template <class Release>
+template <bool kCluster, class Release>
 __device__ __forceinline__ void split_epilogue(const TcConfig& cfg, const TcWork& it, uint8_t* region, uint32_t taddr,
-                                               int lane_base, bool swap, bool f32, Release release) {
+                                               int lane_base, bool swap, bool f32, Release release, float* csmem) {
   const int lane = threadIdx.x & 31;
   const int quad = lane_base >> 5;
+  if (kCluster) {
+    // On-chip mode: the splits of a tile are the CTAs of one cluster, one item
+    // each. This split's fp32 partial goes to this CTA's (now idle) operand
+    // ring, [quad][chunk][32 cols][32 lanes]; cluster_reduce sums the cluster's
+    // partials after the kernel's closing cluster barrier.
+    for (int c0 = 0; c0 < it.col_len; c0 += 32) {
+      uint32_t raw[32];
+      tmem_ld_32x32b_x32(taddr + c0, raw);
+      tmem_ld_wait();
+      float* dst = csmem + ((quad * 4 + (c0 >> 5)) * 32) * 32 + lane;  // <= 4 chunks (n_mma <= 128): 64 KiB
+#pragma unroll
+      for (int e = 0; e < 32; ++e) dst[e * 32] = __uint_as_float(raw[e]);
+    }
+    release();
+    return;
+  }
   const int nsplit = split_n(it.pack), me = split_idx(it.pack), tile = it.c_bs;
   // workspace: [tile][split][quad][chunk][32 cols][32 lanes] — every access is
   // one coalesced 128-B row per register index
@@ -170,7 +186,57 @@ __device__ __forceinline__ void split_epilogue(const TcConfig& cfg, const TcWork
   }
 }
 
-template <int S>
+// On-chip split-K reduction (cfg.cluster_split > 1): CTA `rank` of the
+// cluster sums chunks rank, rank + s, ... of its lane quadrant over the s
+// partials held in the cluster's shared memories (distributed shared memory,
+// fixed split order: deterministic), then applies the fused epilogue op and
+// stores C through the coalesced predicated path.
+__device__ __forceinline__ void cluster_reduce(const TcConfig& cfg, const TcWork& it, uint8_t* region, float* csmem,
+                                               int quad) {
+  const int lane = threadIdx.x & 31;
+  const int lane_base = quad * 32;
+  if (lane_base >= it.lane_len) return;
+  const bool swap = it.flags & kFlagSwap, f32 = it.flags & kFlagOutF32;
+  const int s = cfg.cluster_split;
+  const int rank = static_cast<int>(cluster_ctarank());
+  float* tb = reinterpret_cast<float*>(region);
+  if (lane == 0) bulk_wait_read<0>();  // the transpose tile aliases this warp's store boxes
+  __syncwarp();
+  const int nch = (it.col_len + 31) >> 5;
+  for (int ch = rank; ch < nch; ch += s) {
+    float v[32];
+#pragma unroll
+    for (int e = 0; e < 32; ++e) v[e] = 0.f;
+    const uint32_t mine = smem_addr(csmem + ((quad * 4 + ch) * 32) * 32 + lane);
+    for (int p = 0; p < s; ++p) {
+      const uint32_t pa = mapa_shared(mine, static_cast<uint32_t>(p));
+      float a[32];
+#pragma unroll
+      for (int e = 0; e < 32; ++e) a[e] = ld_dsmem_f32(pa + e * 128);
+#pragma unroll
+      for (int e = 0; e < 32; ++e) v[e] += a[e];
+    }
+    const int c0 = ch * 32;
+    if (it.flags & kFlagEpiOp) {
+      uint32_t rb[32];
+#pragma unroll
+      for (int e = 0; e < 32; ++e) rb[e] = __float_as_uint(v[e]);
+      apply_epi(rb, it.maps->epi, !swap, swap ? it.lane0 + lane_base : it.col0 + c0);
+#pragma unroll
+      for (int e = 0; e < 32; ++e) v[e] = __uint_as_float(rb[e]);
+    }
+    const int ncol = min(32, it.col_len - c0);
+    const int nlane = min(32, it.lane_len - lane_base);
+    if (!swap)
+      store_block32(tb, v, true, it.C, it.ldc, it.lane0 + lane_base, it.col0 + c0, nlane, ncol, f32);
+    else
+      store_block32(tb, v, false, it.C, it.ldc, it.col0 + c0, it.lane0 + lane_base, ncol, nlane, f32);
+  }
+}
+
+// kCluster: the on-chip split-K variant (cluster launch, one item per CTA);
+// a separate instantiation so the common kernel carries none of its code.
+template <int S, bool kCluster>
 __global__ void __launch_bounds__(kTcThreads, 1)
     ftb_tc_kernel(const TcWork* __restrict__ work, int32_t n_work, TcConfig cfg) {
   extern __shared__ uint8_t smem_raw[];
@@ -449,7 +515,7 @@ __global__ void __launch_bounds__(kTcThreads, 1)
         if (lane == 0) mbar_arrive(&tempty[slot]);
       };
       if (it.flags & kFlagSplitK) {
-        split_epilogue(cfg, it, region, taddr, lane_base, swap, f32, release);
+        split_epilogue<kCluster>(cfg, it, region, taddr, lane_base, swap, f32, release, reinterpret_cast<float*>(smem));
       } else if (!it.pack) {
         epilogue_tile(region, ngrp, taddr, lane_base < it.lane_len, tma, swap, f32, &it.maps->out, it.C, it.ldc,
                       it.lane0, it.lane_len, lane_base, it.col0, it.col_len, it.batch, release,
@@ -477,6 +543,13 @@ __global__ void __launch_bounds__(kTcThreads, 1)
 
   tc_fence_before();
   __syncthreads();
+  if (kCluster) {  // one item per CTA: reduce the cluster's split-K partials on chip
+    cluster_sync();              // every split's partial written (release / acquire at cluster scope)
+    if (warp >= 2 && static_cast<int>(blockIdx.x) < n_work)
+      cluster_reduce(cfg, load_work(work, blockIdx.x), reinterpret_cast<uint8_t*>(epi_buf) + (warp & 3) * kEpiWarpBytes,
+                     reinterpret_cast<float*>(smem), warp & 3);
+    cluster_sync();              // peers have read this CTA's partial before it exits
+  }
 #ifdef FTB_TRACE
   if (threadIdx.x == 0 && cfg.trace)  // CTA end stamp (all epilogue stores issued and complete)
     cfg.trace[static_cast<size_t>(blockIdx.x) * kTracePerCta + kTracePerCta - 1] = globaltimer();
@@ -492,16 +565,23 @@ int tc_smem_bytes(const TcConfig& cfg) {
          (4 * kMaxStages + 2) * 8;
 }
 
-template <int S>
-static cudaError_t launch_tc_s(const TcWork* work, int32_t n_work, int32_t n_ctas, TcConfig cfg,
-                               cudaStream_t stream) {
+template <int S, bool kCluster>
+static cudaError_t launch_tc_sk(const TcWork* work, int32_t n_work, int32_t n_ctas, TcConfig cfg,
+                                cudaStream_t stream) {
   static bool configured = false;
   if (!configured) {
-    cudaError_t e = cudaFuncSetAttribute(ftb_tc_kernel<S>, cudaFuncAttributeMaxDynamicSharedMemorySize, 232448);
+    cudaError_t e = cudaFuncSetAttribute(ftb_tc_kernel<S, kCluster>, cudaFuncAttributeMaxDynamicSharedMemorySize, 232448);
     if (e != cudaSuccess) return e;
     configured = true;
   }
-  return launch_pdl(ftb_tc_kernel<S>, n_ctas, kTcThreads, tc_smem_bytes(cfg), stream, work, n_work, cfg);
+  return launch_pdl_cluster(ftb_tc_kernel<S, kCluster>, n_ctas, kTcThreads, tc_smem_bytes(cfg),
+                            kCluster ? cfg.cluster_split : 1, stream, work, n_work, cfg);
+}
+template <int S>
+static cudaError_t launch_tc_s(const TcWork* work, int32_t n_work, int32_t n_ctas, TcConfig cfg,
+                               cudaStream_t stream) {
+  return cfg.cluster_split > 1 ? launch_tc_sk<S, true>(work, n_work, n_ctas, cfg, stream)
+                               : launch_tc_sk<S, false>(work, n_work, n_ctas, cfg, stream);
 }
 
 cudaError_t launch_tc(const TcWork* work, int32_t n_work, int32_t n_ctas, TcConfig cfg,

@@ -254,3 +254,34 @@ def test_dense_swap_tma_store_origin_aligned(cuda, M):
     torch.cuda.synchronize()
     assert _rel(C, ref) < BF16_TOL
     assert torch.isnan(Cb[:, N:].float()).all()
+
+
+@pytest.mark.parametrize("M,N,K", [(64, 4096, 4096), (300, 768, 1024), (160, 768, 3072)])
+def test_split_k_on_chip_matches_workspace_bitwise(cuda, monkeypatch, M, N, K):
+    """Split-K reduced on chip (a cluster of the splits, distributed shared
+    memory) and through the global fp32 workspace: each deterministic across
+    repeated launches, both within tolerance, and bit-identical whenever both
+    use the same split count (same partials, same summation order)."""
+    from paper_2407_21418_b200.runtime import Planner, dense_instance
+
+    A, B, ref = _dense(M, N, K, "nk", torch.bfloat16, cuda, seed=41)
+    prog = Planner().plan([dense_instance(M, N, K)])[0].program
+    outs, ctas = {}, {}
+    for cl in ("1", "0"):
+        monkeypatch.setenv("FTB_SPLIT_CLUSTER", cl)
+        Cout = torch.full((M, N), float("nan"), dtype=torch.bfloat16, device=cuda)
+        ex = Executable([gemm_desc(A, B, Cout, "nk")], [prog])
+        ex.launch()
+        torch.cuda.synchronize()
+        first = Cout.clone()
+        for _ in range(3):
+            Cout.fill_(float("nan"))
+            ex.launch()
+        torch.cuda.synchronize()
+        assert torch.equal(Cout, first)
+        outs[cl], ctas[cl] = first, ex.info.n_ctas
+        ex.close()
+    for cl in outs:
+        assert _rel(outs[cl], ref) < BF16_TOL
+    if ctas["1"] == ctas["0"]:
+        assert torch.equal(outs["1"], outs["0"])
