@@ -9,6 +9,7 @@ from paper_2407_21418_b200.workloads import Shape
 
 P = 1621.8e12
 def timeit(fn, reps=20):
+    torch.cuda.synchronize()  # launches of one table must not overlap (split-K workspace)
     s = torch.cuda.Stream()
     with torch.cuda.stream(s):
         fn(); fn()
