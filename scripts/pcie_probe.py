@@ -22,3 +22,29 @@ b = n * 2
 for name, fn in (("h2d", h2d), ("d2h", d2h), ("both", both)):
     ms = t(fn)
     print(f"{name}: {ms:.2f} ms  {b / ms / 1e6:.1f} GB/s per direction")
+
+
+# chunked: each direction split into C pieces on C streams (several copy engines)
+def chunked(C):
+    hs = [torch.cuda.Stream() for _ in range(C)]
+    ds = [torch.cuda.Stream() for _ in range(C)]
+    step = (n + C - 1) // C
+
+    def fn():
+        cur = torch.cuda.current_stream()
+        for s in hs + ds:
+            s.wait_stream(cur)
+        for c in range(C):
+            lo, hi = c * step, min(n, (c + 1) * step)
+            with torch.cuda.stream(hs[c]):
+                d_in[lo:hi].copy_(h_in[lo:hi], non_blocking=True)
+            with torch.cuda.stream(ds[c]):
+                h_out[lo:hi].copy_(d_out[lo:hi], non_blocking=True)
+        for s in hs + ds:
+            cur.wait_stream(s)
+    return fn
+
+
+for C in (2, 4, 8):
+    ms = t(chunked(C))
+    print(f"both, {C} chunks per direction: {ms:.2f} ms  {b / ms / 1e6:.1f} GB/s per direction")
