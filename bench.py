@@ -319,7 +319,7 @@ def run_ours(args, rank, world, local):
 
     line = {
         "metric": METRIC, "value": value, "unit": "TFLOP/s", "n_gpus": world, "steps": args.steps,
-        "warmup": w, "ms_per_step": t_max_ms, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "warmup": args.warmup, "warmup_launches": w, "ms_per_step": t_max_ms, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
         "dtype": "bf16", "data": "synthetic (U(-1,1) bf16 activations and weights, seeded per rank)",
         "config": {
             "workload": WORKLOAD, "n_shapes_per_gpu": len(shapes), "shapes_per_step": len(shapes),
