@@ -9,7 +9,9 @@ for spec in os.environ.get("SHAPES", "127 4096 4096;160 768 3072;768 768 3072").
     M, N, K = map(int, spec.split())
     A = torch.randn(M, K, device="cuda").bfloat16(); B = torch.randn(N, K, device="cuda").bfloat16()
     C = torch.empty(M, N, device="cuda", dtype=torch.bfloat16)
-    ex = Executable([gemm_desc(A, B, C, "nk")], [Planner().plan([dense_instance(M, N, K)])[0].program], (A, B, C))
+    orient = int(os.environ.get("ORIENT", "-1"))
+    ex = Executable([gemm_desc(A, B, C, "nk", orientation=orient)], [Planner().plan([dense_instance(M, N, K)])[0].program],
+                    (A, B, C))
     for _ in range(200): ex.launch()
     us = time_launches(lambda s: ex.launch(s), reps=20)
     ref = A.float() @ B.float().t()
