@@ -373,6 +373,7 @@ static void build(ExecImpl& ex, const ftb_gemm_desc* probs, const ftb_program* p
     const int64_t lane_max = ffma ? 64 : kLaneRows;
     const int64_t col_max = ffma ? 64 : kMaxN;
     const int64_t gran = P.col_mn ? 64 : 16;
+    const size_t first_item = items.size();
     for (const Region& r : regs) {
       const int64_t b0 = ib ? r.lo[0] : 0, b1 = ib ? r.hi[0] : 1;
       const int64_t ilo = r.lo[ib], ihi = r.hi[ib], jlo = r.lo[ib + 1], jhi = r.hi[ib + 1];
@@ -406,6 +407,28 @@ static void build(ExecImpl& ex, const ftb_gemm_desc* probs, const ftb_program* p
             items.push_back({cost, w});
             ex.info.mma_flops += 2 * cells * kBlockK;
           }
+    }
+    // Rasterise this problem's items for L2 locality: the persistent CTAs run a
+    // window of ~one item per SM at a time, so order items by column group
+    // (about 32 MiB of the column operand over K), then lane range, then
+    // column: a group's column tiles stay L2-resident while the lane tiles
+    // stream past once per group. Measured on 8192^3: row-major order read
+    // 2.05 GB from DRAM for 0.26 GB of inputs; 32 MiB groups: 1.02 GB, sustained
+    // 1065 -> 1232 TF/s (the power-capped clock rises with less DRAM traffic).
+    if (!ffma) {
+      const int64_t kbytes = std::max<int64_t>(1, d.K * 2);
+      static const int64_t raster_mb = [] {
+        const char* e = std::getenv("FTB_RASTER_MB");
+        return e ? std::max<int64_t>(1, std::atoll(e)) : int64_t(32);
+      }();
+      const int64_t group = std::max<int64_t>(kMaxN, (raster_mb << 20) / kbytes / kMaxN * kMaxN);
+      std::stable_sort(items.begin() + first_item, items.end(), [group](const Keyed& a, const Keyed& b) {
+        if (a.w.batch != b.w.batch) return a.w.batch < b.w.batch;
+        const int64_t ga = a.w.col0 / group, gb = b.w.col0 / group;
+        if (ga != gb) return ga < gb;
+        if (a.w.lane0 != b.w.lane0) return a.w.lane0 < b.w.lane0;
+        return a.w.col0 < b.w.col0;
+      });
     }
     ex.info.true_flops += 2 * d.batch * d.M * d.N * d.K;
     ex.info.covered_out += covered;
