@@ -426,7 +426,9 @@ static void build(ExecImpl& ex, const ftb_gemm_desc* probs, const ftb_program* p
         if (a.w.batch != b.w.batch) return a.w.batch < b.w.batch;
         const int64_t ga = a.w.col0 / group, gb = b.w.col0 / group;
         if (ga != gb) return ga < gb;
-        if (a.w.lane0 != b.w.lane0) return a.w.lane0 < b.w.lane0;
+        // snake: odd groups sweep the lanes backwards, starting on the lane
+        // tiles the previous group left in L2
+        if (a.w.lane0 != b.w.lane0) return (ga & 1) ? a.w.lane0 > b.w.lane0 : a.w.lane0 < b.w.lane0;
         return a.w.col0 < b.w.col0;
       });
     }
