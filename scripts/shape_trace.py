@@ -38,6 +38,11 @@ for spec in os.environ.get("SHAPES", "160 768 768;1376 768 768;160 768 3072").sp
     print(f"M{M} N{N} K{K}: {us:.2f} us/launch (graph x20), {us1:.2f} (x1); items {ex.info.n_work}, ctas {n}, cfg {ex.config()['single']}")
     last = rel[:, :, 5].max()
     print(f"  trace span first pick -> last release {last:.2f} us; pick spread {rel[:n,0,0].min():.2f}..{rel[:n,0,0].max():.2f}")
+    sp = getattr(ex, "trace_span", None)
+    if sp is not None and sp[:n, 1].max() > 0:
+        sp = sp[:n].astype(np.int64)
+        print(f"  CTA start {((sp[:, 0] - t0) / 1e3).min():.2f}..{((sp[:, 0] - t0) / 1e3).max():.2f} us, "
+              f"end p50 {np.median((sp[:, 1] - t0) / 1e3):.2f} max {((sp[:, 1] - t0) / 1e3).max():.2f} us (from first pick)")
     for ev, nm in ((1, "tma0"), (2, "k0land"), (3, "commit"), (4, "epi"), (5, "rel")):
         v = rel[:n, 0, ev]
         print(f"  {nm:7s} min {v.min():.2f} p50 {np.median(v):.2f} max {v.max():.2f}")
