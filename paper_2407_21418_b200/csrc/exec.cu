@@ -729,6 +729,31 @@ static void upload(ExecImpl& I) {
       tw.swap(mix);
     }
   }
+  // Eight epilogue warps for tables of short, narrow items (<= 4 K blocks per
+  // item on average, <= 128-column accumulators, more items than SMs, no
+  // split-K): their epilogue (TMEM -> smem -> TMA store) is the bottleneck
+  // (C2 attention, scripts/bmm_trace.py); two groups of four warps drain
+  // alternate items.
+  {
+    const char* env_e8 = std::getenv("FTB_EPI8");
+    int sms_here = device_sms();
+    if (sms_here <= 0) sms_here = 148;
+    int64_t kb_sum = 0;
+    int32_t widest = 0;
+    bool split = false;
+    for (const TcWork& t : tw) {
+      kb_sum += t.num_kb;
+      widest = std::max(widest, t.n_mma);
+      split = split || (t.flags & kFlagSplitK);
+    }
+    const int64_t n = static_cast<int64_t>(tw.size());
+    // narrow accumulators only: 256-column items need four single-buffered
+    // store groups each and ran slower (C2 scores T=512: 113 -> 123 us);
+    // measured gains: C2 T=64 scores/context 5.7 -> 5.1 us, T=256 context 36.6 -> 34.8 us
+    bool e8 = !pairing && !split && n > sms_here && widest <= 128 && kb_sum <= 4 * n;
+    if (env_e8) e8 = env_e8[0] == '1' && !pairing && !split;
+    I.cfg.epi8 = e8 ? 1 : 0;
+  }
   I.n_singles = static_cast<int64_t>(tw.size());
   I.n_pairs = static_cast<int64_t>(pairs.size());
   if (!tw.empty()) {

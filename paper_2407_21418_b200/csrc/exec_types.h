@@ -138,7 +138,7 @@ struct TcConfig {
   float* split_ws;            // split-K partials [tile][split][128][256] fp32
   int32_t* split_cnt;         // split-K counters [tile][arrive, depart][4 lane quadrants]
   int32_t cluster_split;      // > 1: split-K partials reduced on chip across a cluster of this many CTAs
-  int32_t pad_;
+  int32_t epi8;               // 1: eight epilogue warps (two groups on alternate items), 320 threads
 };
 constexpr int kTraceItems = 16;   // items traced per CTA
 constexpr int kTraceEvents = 6;   // see kernel_tc.cu
@@ -153,6 +153,7 @@ constexpr int kMmaFloorN = 200;      // an M=128 K=16 tcgen05.mma costs >= ~100 
 constexpr int kLaneStageBytes = kLaneRows * kBlockK * 2;   // 16 KiB
 constexpr int kTmemCols = 512;
 constexpr int kTcThreads = 192;                            // 6 warps
+constexpr int kTcThreadsEpi8 = 320;                        // 10 warps: eight epilogue warps
 constexpr int kEpiWarpBytes = 8192;   // per epilogue warp: four 2 KiB bf16 TMA store boxes, or (aliased)
                                        // the 32x33 fp32 transpose tile of the predicated path
 constexpr int kEpiStageBytes = 4 * kEpiWarpBytes;

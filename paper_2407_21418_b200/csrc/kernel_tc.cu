@@ -235,9 +235,11 @@ __device__ __forceinline__ void cluster_reduce(const TcConfig& cfg, const TcWork
 }
 
 // kCluster: the on-chip split-K variant (cluster launch, one item per CTA);
-// a separate instantiation so the common kernel carries none of its code.
-template <int S, bool kCluster>
-__global__ void __launch_bounds__(kTcThreads, 1)
+// kEpi8: eight epilogue warps (tables of short items, epilogue bound;
+// 320 threads at a 168-register budget). Separate instantiations, so the
+// common kernel carries none of their code.
+template <int S, bool kCluster, bool kEpi8>
+__global__ void __launch_bounds__(kEpi8 ? 384 : kTcThreads, 1)
     ftb_tc_kernel(const TcWork* __restrict__ work, int32_t n_work, TcConfig cfg) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
@@ -483,17 +485,23 @@ __global__ void __launch_bounds__(kTcThreads, 1)
     // ------------------------------------------------------------ epilogue
     const int quad = warp & 3;  // TMEM lane quadrant this warp may access
     // per-warp 8 KiB staging region: four 2 KiB TMA store boxes (two groups of
-    // two), or — for predicated items — the 32x33 fp32 transpose tile (aliased)
-    uint8_t* region = reinterpret_cast<uint8_t*>(epi_buf) + quad * kEpiWarpBytes;
-    uint32_t local = 0, ngrp = 0;
+    // two), or — for predicated items — the 32x33 fp32 transpose tile (aliased).
+    // kEpi8: two groups of four warps take alternate items (alternate TMEM
+    // slots), 4 KiB each, so two items' epilogues run concurrently.
+    const int egrp = kEpi8 ? (warp - 2) >> 2 : 0;
+    uint8_t* region = reinterpret_cast<uint8_t*>(epi_buf) +
+                      (kEpi8 ? (warp - 2) * (kEpiWarpBytes / 2) : quad * kEpiWarpBytes);
+    const int step = kEpi8 ? 2 : 1;
+    uint32_t local = egrp, ngrp = 0;
 #ifdef FTB_PROD_PROFILE
     unsigned long long e_wait = 0, e_t0 = clock64();
 #endif
     TcWork nxt;
-    if (static_cast<int>(blockIdx.x) < n_work) nxt = load_work(work, blockIdx.x);
-    for (int w = blockIdx.x; w < n_work; w += G, ++local) {
+    const int w0 = static_cast<int>(blockIdx.x) + egrp * G;
+    if (w0 < n_work) nxt = load_work(work, w0);
+    for (int w = w0; w < n_work; w += step * G, local += step) {
       const TcWork it = nxt;
-      if (w + G < n_work) nxt = load_work(work, w + G);
+      if (w + step * G < n_work) nxt = load_work(work, w + step * G);
       const uint32_t slot = local % cfg.n_acc;
       const uint32_t use = local / cfg.n_acc;
       const bool swap = it.flags & kFlagSwap, f32 = it.flags & kFlagOutF32;
@@ -517,15 +525,15 @@ __global__ void __launch_bounds__(kTcThreads, 1)
       if (it.flags & kFlagSplitK) {
         split_epilogue<kCluster>(cfg, it, region, taddr, lane_base, swap, f32, release, reinterpret_cast<float*>(smem));
       } else if (!it.pack) {
-        epilogue_tile(region, ngrp, taddr, lane_base < it.lane_len, tma, swap, f32, &it.maps->out, it.C, it.ldc,
-                      it.lane0, it.lane_len, lane_base, it.col0, it.col_len, it.batch, release,
-                      (it.flags & kFlagEpiOp) ? &it.maps->epi : nullptr);
+        epilogue_tile<kEpi8>(region, ngrp, taddr, lane_base < it.lane_len, tma, swap, f32, &it.maps->out, it.C,
+                             it.ldc, it.lane0, it.lane_len, lane_base, it.col0, it.col_len, it.batch, release,
+                             (it.flags & kFlagEpiOp) ? &it.maps->epi : nullptr);
       } else {
         // block-diagonal pack: this warp's lane quadrant belongs to entry e
         const int wpe = pack_lane_rows(it.pack) / 32;  // warps per entry
         const int e = quad / wpe, r0 = (quad % wpe) * 32;
         const bool active = e < pack_nb(it.pack) && r0 < it.lane_len;
-        epilogue_tile(region, ngrp, taddr + e * 64, active, tma, swap, f32, &it.maps->out,
+        epilogue_tile<kEpi8>(region, ngrp, taddr + e * 64, active, tma, swap, f32, &it.maps->out,
                       static_cast<char*>(it.C) + static_cast<size_t>(e) * it.c_bs * (f32 ? 4 : 2), it.ldc, 0,
                       it.lane_len, r0, 0, it.col_len, it.batch + e, release);
       }
@@ -565,23 +573,25 @@ int tc_smem_bytes(const TcConfig& cfg) {
          (4 * kMaxStages + 2) * 8;
 }
 
-template <int S, bool kCluster>
+template <int S, bool kCluster, bool kEpi8>
 static cudaError_t launch_tc_sk(const TcWork* work, int32_t n_work, int32_t n_ctas, TcConfig cfg,
                                 cudaStream_t stream) {
   static bool configured = false;
   if (!configured) {
-    cudaError_t e = cudaFuncSetAttribute(ftb_tc_kernel<S, kCluster>, cudaFuncAttributeMaxDynamicSharedMemorySize, 232448);
+    cudaError_t e = cudaFuncSetAttribute(ftb_tc_kernel<S, kCluster, kEpi8>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         232448);
     if (e != cudaSuccess) return e;
     configured = true;
   }
-  return launch_pdl_cluster(ftb_tc_kernel<S, kCluster>, n_ctas, kTcThreads, tc_smem_bytes(cfg),
-                            kCluster ? cfg.cluster_split : 1, stream, work, n_work, cfg);
+  return launch_pdl_cluster(ftb_tc_kernel<S, kCluster, kEpi8>, n_ctas, kEpi8 ? kTcThreadsEpi8 : kTcThreads,
+                            tc_smem_bytes(cfg), kCluster ? cfg.cluster_split : 1, stream, work, n_work, cfg);
 }
 template <int S>
 static cudaError_t launch_tc_s(const TcWork* work, int32_t n_work, int32_t n_ctas, TcConfig cfg,
                                cudaStream_t stream) {
-  return cfg.cluster_split > 1 ? launch_tc_sk<S, true>(work, n_work, n_ctas, cfg, stream)
-                               : launch_tc_sk<S, false>(work, n_work, n_ctas, cfg, stream);
+  if (cfg.cluster_split > 1) return launch_tc_sk<S, true, false>(work, n_work, n_ctas, cfg, stream);
+  if (cfg.epi8) return launch_tc_sk<S, false, true>(work, n_work, n_ctas, cfg, stream);
+  return launch_tc_sk<S, false, false>(work, n_work, n_ctas, cfg, stream);
 }
 
 cudaError_t launch_tc(const TcWork* work, int32_t n_work, int32_t n_ctas, TcConfig cfg,

@@ -285,3 +285,38 @@ def test_split_k_on_chip_matches_workspace_bitwise(cuda, monkeypatch, M, N, K):
         assert _rel(outs[cl], ref) < BF16_TOL
     if ctas["1"] == ctas["0"]:
         assert torch.equal(outs["1"], outs["0"])
+
+
+@pytest.mark.parametrize("case", ["scores64", "context256", "dense_f32"])
+def test_eight_warp_epilogue_bitwise_equal(cuda, monkeypatch, case):
+    """The eight-epilogue-warp kernel (two warp groups on alternate items,
+    4 KiB staging, half-tile transpose) writes exactly the bits of the common
+    kernel: forced on and off over a packed BMM, an unpacked BMM and a Dense
+    table with fp32 outputs (predicated store path)."""
+    from paper_2407_21418_b200.runtime import Planner, bmm_instance, dense_instance
+
+    g = torch.Generator(device="cpu").manual_seed(7)
+    if case == "scores64":
+        A = (torch.rand(300, 64, 64, generator=g) * 2 - 1).bfloat16().to(cuda)
+        B = (torch.rand(300, 64, 64, generator=g) * 2 - 1).bfloat16().to(cuda)
+        shape, lay, inst, dt = (300, 64, 64), "nk", bmm_instance(300, 64, 64, 64), torch.bfloat16
+    elif case == "context256":
+        A = (torch.rand(200, 256, 256, generator=g) * 2 - 1).bfloat16().to(cuda)
+        B = (torch.rand(200, 256, 72, generator=g) * 2 - 1).bfloat16().to(cuda)[:, :, :70]
+        shape, lay, inst, dt = (200, 256, 70), "kn", bmm_instance(200, 256, 70, 256, ("i", "k")), torch.bfloat16
+    else:
+        A = (torch.rand(3000, 64, generator=g) * 2 - 1).bfloat16().to(cuda)
+        B = (torch.rand(100, 64, generator=g) * 2 - 1).bfloat16().to(cuda)
+        shape, lay, inst, dt = (3000, 100), "nk", dense_instance(3000, 100, 64), torch.float32
+    prog = Planner().plan([inst])[0].program
+    outs = []
+    for e8 in ("0", "1"):
+        monkeypatch.setenv("FTB_EPI8", e8)
+        C = torch.full(shape, float("nan"), dtype=dt, device=cuda)
+        ex = Executable([gemm_desc(A, B, C, lay)], [prog])
+        ex.launch()
+        torch.cuda.synchronize()
+        outs.append(C.clone())
+        ex.close()
+    assert not torch.isnan(outs[0].float()).any()
+    assert torch.equal(outs[0], outs[1])
