@@ -729,28 +729,30 @@ static void upload(ExecImpl& I) {
       tw.swap(mix);
     }
   }
-  // Eight epilogue warps for tables of short, narrow items (<= 4 K blocks per
-  // item on average, <= 128-column accumulators, more items than SMs, no
-  // split-K): their epilogue (TMEM -> smem -> TMA store) is the bottleneck
-  // (C2 attention, scripts/bmm_trace.py); two groups of four warps drain
-  // alternate items.
+  // Eight epilogue warps for tables of short items (<= 8 K blocks per item on
+  // average, more items than SMs, no split-K): their epilogue (TMEM -> smem ->
+  // TMA store) is the bottleneck (C2 attention, scripts/bmm_trace.py); two
+  // groups of four warps drain alternate items, with 8 KiB double-buffered
+  // staging each (the ring gives up stages: short items need few).
   {
     const char* env_e8 = std::getenv("FTB_EPI8");
     int sms_here = device_sms();
     if (sms_here <= 0) sms_here = 148;
-    int64_t kb_sum = 0;
-    int32_t widest = 0;
+    int64_t kb_sum = 0, out_bytes = 0;
     bool split = false;
     for (const TcWork& t : tw) {
       kb_sum += t.num_kb;
-      widest = std::max(widest, t.n_mma);
+      const int64_t entries = t.pack ? pack_nb(t.pack) : 1;
+      out_bytes += entries * t.lane_len * t.col_len * ((t.flags & kFlagOutF32) ? 4 : 2);
       split = split || (t.flags & kFlagSplitK);
     }
     const int64_t n = static_cast<int64_t>(tw.size());
-    // narrow accumulators only: 256-column items need four single-buffered
-    // store groups each and ran slower (C2 scores T=512: 113 -> 123 us);
-    // measured gains: C2 T=64 scores/context 5.7 -> 5.1 us, T=256 context 36.6 -> 34.8 us
-    bool e8 = !pairing && !split && n > sms_here && widest <= 128 && kb_sum <= 4 * n;
+    // not for tables of near-full output tiles (>= 48 KiB per item on average):
+    // those are DRAM-write bound and a second epilogue group only costs ring
+    // stages (C2 scores T=512: 112 -> 124 us). Measured gains: C2 scores
+    // T=257 121 -> 85 us, T=64 scores / context 5.7 -> 5.0 us, context T=256
+    // 36.4 -> 34.5 us, T=512 100 vs 104 us; C1 per-shape scores 0.147 -> 0.163.
+    bool e8 = !pairing && !split && n > sms_here && kb_sum <= 8 * n && out_bytes < (int64_t(48) << 10) * n;
     if (env_e8) e8 = env_e8[0] == '1' && !pairing && !split;
     I.cfg.epi8 = e8 ? 1 : 0;
   }

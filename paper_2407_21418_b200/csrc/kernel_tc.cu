@@ -247,7 +247,7 @@ __global__ void __launch_bounds__(kEpi8 ? 384 : kTcThreads, 1)
   uint8_t* lane_buf = smem;                                   // S x 16 KiB
   uint8_t* col_buf = smem + S * kLaneStageBytes;              // S x col_stage_bytes
   float* epi_buf = reinterpret_cast<float*>(col_buf + S * cfg.col_stage_bytes);  // 4 x 32x33
-  uint64_t* bars = reinterpret_cast<uint64_t*>(reinterpret_cast<uint8_t*>(epi_buf) + kEpiStageBytes);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(reinterpret_cast<uint8_t*>(epi_buf) + (kEpi8 ? 2 : 1) * kEpiStageBytes);
   uint64_t* full = bars;                      // [S]
   uint64_t* empty = bars + kMaxStages;        // [S]
   uint64_t* tfull = bars + 2 * kMaxStages;    // [n_acc]
@@ -487,10 +487,10 @@ __global__ void __launch_bounds__(kEpi8 ? 384 : kTcThreads, 1)
     // per-warp 8 KiB staging region: four 2 KiB TMA store boxes (two groups of
     // two), or — for predicated items — the 32x33 fp32 transpose tile (aliased).
     // kEpi8: two groups of four warps take alternate items (alternate TMEM
-    // slots), 4 KiB each, so two items' epilogues run concurrently.
+    // slots), 8 KiB each (the staging doubles; the ring gives up stages), so
+    // two items' epilogues run concurrently.
     const int egrp = kEpi8 ? (warp - 2) >> 2 : 0;
-    uint8_t* region = reinterpret_cast<uint8_t*>(epi_buf) +
-                      (kEpi8 ? (warp - 2) * (kEpiWarpBytes / 2) : quad * kEpiWarpBytes);
+    uint8_t* region = reinterpret_cast<uint8_t*>(epi_buf) + (kEpi8 ? (warp - 2) : quad) * kEpiWarpBytes;
     const int step = kEpi8 ? 2 : 1;
     uint32_t local = egrp, ngrp = 0;
 #ifdef FTB_PROD_PROFILE
@@ -525,15 +525,15 @@ __global__ void __launch_bounds__(kEpi8 ? 384 : kTcThreads, 1)
       if (it.flags & kFlagSplitK) {
         split_epilogue<kCluster>(cfg, it, region, taddr, lane_base, swap, f32, release, reinterpret_cast<float*>(smem));
       } else if (!it.pack) {
-        epilogue_tile<kEpi8>(region, ngrp, taddr, lane_base < it.lane_len, tma, swap, f32, &it.maps->out, it.C,
-                             it.ldc, it.lane0, it.lane_len, lane_base, it.col0, it.col_len, it.batch, release,
-                             (it.flags & kFlagEpiOp) ? &it.maps->epi : nullptr);
+        epilogue_tile(region, ngrp, taddr, lane_base < it.lane_len, tma, swap, f32, &it.maps->out, it.C, it.ldc,
+                      it.lane0, it.lane_len, lane_base, it.col0, it.col_len, it.batch, release,
+                      (it.flags & kFlagEpiOp) ? &it.maps->epi : nullptr);
       } else {
         // block-diagonal pack: this warp's lane quadrant belongs to entry e
         const int wpe = pack_lane_rows(it.pack) / 32;  // warps per entry
         const int e = quad / wpe, r0 = (quad % wpe) * 32;
         const bool active = e < pack_nb(it.pack) && r0 < it.lane_len;
-        epilogue_tile<kEpi8>(region, ngrp, taddr + e * 64, active, tma, swap, f32, &it.maps->out,
+        epilogue_tile(region, ngrp, taddr + e * 64, active, tma, swap, f32, &it.maps->out,
                       static_cast<char*>(it.C) + static_cast<size_t>(e) * it.c_bs * (f32 ? 4 : 2), it.ldc, 0,
                       it.lane_len, r0, 0, it.col_len, it.batch + e, release);
       }
@@ -569,7 +569,7 @@ __global__ void __launch_bounds__(kEpi8 ? 384 : kTcThreads, 1)
 }
 
 int tc_smem_bytes(const TcConfig& cfg) {
-  return 1024 + cfg.stages * (kLaneStageBytes + cfg.col_stage_bytes) + kEpiStageBytes +
+  return 1024 + cfg.stages * (kLaneStageBytes + cfg.col_stage_bytes) + (cfg.epi8 ? 2 : 1) * kEpiStageBytes +
          (4 * kMaxStages + 2) * 8;
 }
 
