@@ -53,10 +53,10 @@ __device__ __forceinline__ void store_row32(void* C, int64_t off, const float* v
 // Store a 32 x 32 fp32 block that a warp holds in registers — one ROW of C
 // per lane (lane_is_row) or one COLUMN of C per lane — to C[row0.., col0..]
 // (clipped to nrows x ncols). The block goes through a padded smem tile
-// (32 x 33 fp32, conflict-free both ways; kHalf: two passes of 16 x 33 for a
-// 4 KiB staging region); each lane then writes 8 consecutive elements of one
-// row per pass, so one warp store instruction covers 8 rows x 8 elements x 4
-// lanes = 8 full 64-B (bf16) row segments instead of 32 scattered 16-B pieces.
+// (32 x 33 fp32, conflict-free both ways); each lane then writes 8
+// consecutive elements of one row per pass, so one warp store instruction
+// covers 8 rows x 8 elements x 4 lanes = 8 full 64-B (bf16) row segments
+// instead of 32 scattered 16-B pieces.
 __device__ __forceinline__ void store_rows8(const float* tb, int rl, int r, int cq, void* C, int64_t ldc,
                                            int64_t row0, int64_t col0, int nrows, int ncols, bool f32) {
   if (r < nrows && cq < ncols) {
@@ -95,48 +95,25 @@ __device__ __forceinline__ void store_rows8(const float* tb, int rl, int r, int 
   }
 }
 
-template <bool kHalf = false>
 __device__ __forceinline__ void store_block32(float* tb, const float (&v)[32], bool lane_is_row, void* C,
                                               int64_t ldc, int64_t row0, int64_t col0, int nrows, int ncols,
                                               bool f32) {
   const int lane = threadIdx.x & 31;
   const int cq = (lane & 3) * 8;
-  if (!kHalf) {
-    if (lane_is_row) {
+  if (lane_is_row) {
 #pragma unroll
-      for (int x = 0; x < 32; ++x) tb[lane * 33 + x] = v[x];
-    } else {
-#pragma unroll
-      for (int x = 0; x < 32; ++x) tb[x * 33 + lane] = v[x];
-    }
-    __syncwarp();
-#pragma unroll
-    for (int p = 0; p < 4; ++p) {
-      const int r = (lane >> 2) + 8 * p;
-      store_rows8(tb, r, r, cq, C, ldc, row0, col0, nrows, ncols, f32);
-    }
-    __syncwarp();
+    for (int x = 0; x < 32; ++x) tb[lane * 33 + x] = v[x];
   } else {
 #pragma unroll
-    for (int h = 0; h < 2; ++h) {
-      if (lane_is_row) {
-        if ((lane >> 4) == h) {
-#pragma unroll
-          for (int x = 0; x < 32; ++x) tb[(lane & 15) * 33 + x] = v[x];
-        }
-      } else {
-#pragma unroll
-        for (int x = 0; x < 16; ++x) tb[x * 33 + lane] = v[16 * h + x];
-      }
-      __syncwarp();
-#pragma unroll
-      for (int p = 0; p < 2; ++p) {
-        const int rl = (lane >> 2) + 8 * p;
-        store_rows8(tb, rl, 16 * h + rl, cq, C, ldc, row0, col0, nrows, ncols, f32);
-      }
-      __syncwarp();
-    }
+    for (int x = 0; x < 32; ++x) tb[x * 33 + lane] = v[x];
   }
+  __syncwarp();
+#pragma unroll
+  for (int p = 0; p < 4; ++p) {
+    const int r = (lane >> 2) + 8 * p;
+    store_rows8(tb, r, r, cq, C, ldc, row0, col0, nrows, ncols, f32);
+  }
+  __syncwarp();
 }
 
 __device__ __forceinline__ unsigned long long globaltimer() {
@@ -236,9 +213,7 @@ __device__ unsigned long long* ftb_epi_dbg;
   } while (0)
 #endif
 
-// kSingleBuf: 4 KiB staging per warp (one group of two boxes; the eight-warp
-// epilogue variant) instead of 8 KiB double-buffered groups.
-template <bool kSingleBuf = false, class Release>
+template <class Release>
 __device__ __forceinline__ void epilogue_tile(uint8_t* region, uint32_t& ngrp, uint32_t taddr, bool active, bool tma,
                                               bool swap, bool f32, const CUtensorMap* out_map, void* C, int64_t ldc,
                                               int lane0, int lane_len, int lane_base, int col0, int col_len, int batch,
@@ -264,11 +239,8 @@ __device__ __forceinline__ void epilogue_tile(uint8_t* region, uint32_t& ngrp, u
           apply_epi(ra, *op, !swap, swap ? lane0 + lane_base : col0 + c0);
           if (two) apply_epi(rb, *op, !swap, swap ? lane0 + lane_base : col0 + c0 + 32);
         }
-        uint8_t* box = kSingleBuf ? region : region + (ngrp & 1) * 4096;
-        if (lane == 0) {  // the group that last used these boxes has read them
-          if (kSingleBuf) bulk_wait_read<0>();
-          else bulk_wait_read<1>();
-        }
+        uint8_t* box = region + (ngrp & 1) * 4096;
+        if (lane == 0) bulk_wait_read<1>();  // the group that last used these boxes has read them
         __syncwarp();
         FTB_EPI_EV((c0 >> 6) * 6 + 1);
         stage_box_bf16(box, ra, !swap);
@@ -307,9 +279,9 @@ __device__ __forceinline__ void epilogue_tile(uint8_t* region, uint32_t& ngrp, u
         const int ncol = min(32, col_len - c0);
         const int nlane = min(32, lane_len - lane_base);
         if (!swap)  // lanes = rows of C, TMEM columns = output columns
-          store_block32<kSingleBuf>(tb, v, true, C, ldc, lane0 + lane_base, col0 + c0, nlane, ncol, f32);
+          store_block32(tb, v, true, C, ldc, lane0 + lane_base, col0 + c0, nlane, ncol, f32);
         else        // lanes = columns of C, TMEM columns = output rows
-          store_block32<kSingleBuf>(tb, v, false, C, ldc, col0 + c0, lane0 + lane_base, ncol, nlane, f32);
+          store_block32(tb, v, false, C, ldc, col0 + c0, lane0 + lane_base, ncol, nlane, f32);
       }
     }
   }
