@@ -8,7 +8,10 @@
 // Both CTAs of a cluster use the same B rows, so MODE=1 moves 1/3 fewer bytes
 // from L2 for the same MMAs. Run each mode alone for ~2 s while sampling SM
 // clocks (nvidia-smi) to compare sustained TF/s under the power cap.
-// Usage: MODE=0|1 SECS=2 ./mcast_bench
+//   MODE=2: one CTA computes a 256x256 tile (two 128-lane accumulators of 256
+//           columns): A 256 rows + B 256 rows per 64-wide K block (64 KiB,
+//           3 stages), 8 MMAs per K block: 1/3 fewer staged bytes per flop
+// Usage: MODE=0|1|2 SECS=2 ./mcast_bench
 #include <cuda.h>
 #include <cudaTypedefs.h>
 #include <cuda_runtime.h>
@@ -36,7 +39,7 @@ __device__ __forceinline__ void tc_commit_mc1(uint64_t* bar) {
 
 template <int MODE>
 __global__ void __launch_bounds__(128, 1) mcast_kernel(const __grid_constant__ Maps maps, int iters, int R) {
-  constexpr int S = 4, kA = 128 * 128, kB = 256 * 128, kStage = kA + kB;
+  constexpr int S = MODE == 2 ? 3 : 4, kA = (MODE == 2 ? 256 : 128) * 128, kB = 256 * 128, kStage = kA + kB;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + S * kStage);
@@ -46,7 +49,7 @@ __global__ void __launch_bounds__(128, 1) mcast_kernel(const __grid_constant__ M
   const uint32_t rank = cluster_ctarank();
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
   if (threadIdx.x == 0) {
-    for (int s = 0; s < S; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], MODE ? 2 : 1); }
+    for (int s = 0; s < S; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], MODE == 1 ? 2 : 1); }
     mbar_init(done, 1);
     fence_barrier_init();
   }
@@ -68,7 +71,10 @@ __global__ void __launch_bounds__(128, 1) mcast_kernel(const __grid_constant__ M
       const int brow = 4096 + (cluster % 8) * 256;
       mbar_arrive_expect_tx(&full[ps], kStage);
       tma_load_3d(dst, &maps.a, &full[ps], k0, arow, 0);
-      if (MODE == 0) {
+      if (MODE == 2) {
+        tma_load_3d(dst + 128 * 128, &maps.a, &full[ps], k0, arow + 2048, 0);
+        tma_load_3d(dst + kA, &maps.bf, &full[ps], k0, brow, 0);
+      } else if (MODE == 0) {
         tma_load_3d(dst + kA, &maps.bf, &full[ps], k0, brow, 0);
       } else {
         tma_load_3d_mc(dst + kA + rank * (kB / 2), &maps.bh, &full[ps], k0, brow + rank * 128, 0);
@@ -82,10 +88,14 @@ __global__ void __launch_bounds__(128, 1) mcast_kernel(const __grid_constant__ M
       mbar_wait(&full[cs], ph);
       tc_fence_after();
       const uint32_t la = smem_addr(smem + cs * kStage), ca = la + kA;
-      for (int kk = 0; kk < 4; ++kk)
+      for (int kk = 0; kk < 4; ++kk) {
         tc_mma_f16(tmem, umma_desc_sw128(la + kk * 32, 16, 1024), umma_desc_sw128(ca + kk * 32, 16, 1024), idesc,
                    (it | kk) != 0);
-      if (MODE) tc_commit_mc1(&empty[cs]); else tc_commit(&empty[cs]);
+        if (MODE == 2)  // second 128-lane half of the 256-row A tile into the second accumulator
+          tc_mma_f16(tmem + 256, umma_desc_sw128(la + 16384 + kk * 32, 16, 1024),
+                     umma_desc_sw128(ca + kk * 32, 16, 1024), idesc, (it | kk) != 0);
+      }
+      if (MODE == 1) tc_commit_mc1(&empty[cs]); else tc_commit(&empty[cs]);
       if (++cs == S) { cs = 0; ph ^= 1; }
     }
     tc_commit(done);
@@ -133,14 +143,14 @@ int main() {
   make(&m.bh, buf, K, R, 128);
   make(&m.bf, buf, K, R, 256);
   const int ctas = 148, iters = 4096;  // 64 tiles of K=4096 per CTA per launch
-  const int smem = 4 * (128 + 256) * 128 + 2048;
+  const int smem = (mode == 2 ? 3 * (256 + 256) : 4 * (128 + 256)) * 128 + 2048;
   cudaLaunchConfig_t lc = {};
   lc.gridDim = dim3(ctas); lc.blockDim = dim3(128); lc.dynamicSmemBytes = smem;
   cudaLaunchAttribute at[1];
   at[0].id = cudaLaunchAttributeClusterDimension;
   at[0].val.clusterDim.x = 2; at[0].val.clusterDim.y = 1; at[0].val.clusterDim.z = 1;
   lc.attrs = at; lc.numAttrs = 1;
-  auto kern = mode ? mcast_kernel<1> : mcast_kernel<0>;
+  auto kern = mode == 2 ? mcast_kernel<2> : (mode ? mcast_kernel<1> : mcast_kernel<0>);
   cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   cudaError_t e = cudaLaunchKernelEx(&lc, kern, m, 64, (int)R);
   cudaDeviceSynchronize();
@@ -154,7 +164,7 @@ int main() {
     float ms; cudaEventElapsedTime(&ms, e0, e1);
     total_ms += ms; launches += 10;
   }
-  const double flops = 2.0 * 128 * 256 * 64 * (double)iters * ctas * launches;
+  const double flops = (mode == 2 ? 2.0 : 1.0) * 2.0 * 128 * 256 * 64 * (double)iters * ctas * launches;
   printf("MODE=%d err=%d: %d launches in %.0f ms: %.0f TF/s (%.1f us/launch)\n", mode, (int)e, launches, total_ms,
          flops / (total_ms * 1e-3) / 1e12, total_ms * 1e3 / launches);
   return 0;

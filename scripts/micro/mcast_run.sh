@@ -1,6 +1,6 @@
 # Run mcast_bench MODE 0/1 alternately, each ~2.5 s, with SM clock / power sampling (median of the in-run samples)
 cd "$(dirname "$0")"
-for r in 1 2; do for m in 0 1; do
+for r in 1 2; do for m in ${MODES:-0 1}; do
   nvidia-smi --query-gpu=clocks.sm,power.draw --format=csv,noheader,nounits -lms 100 > /tmp/clk_$m.txt &
   SPID=$!
   sleep 0.3
