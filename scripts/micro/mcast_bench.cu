@@ -11,7 +11,9 @@
 //   MODE=2: one CTA computes a 256x256 tile (two 128-lane accumulators of 256
 //           columns): A 256 rows + B 256 rows per 64-wide K block (64 KiB,
 //           3 stages), 8 MMAs per K block: 1/3 fewer staged bytes per flop
-// Usage: MODE=0|1|2 SECS=2 ./mcast_bench
+//   MODE=3: CTA pair (tcgen05 cta_group::2, M=256 N=256 per pair): each CTA
+//           stages its 128 A rows + half of B (32 KiB), the leader issues
+// Usage: MODE=0|1|2|3 SECS=2 ./mcast_bench
 #include <cuda.h>
 #include <cudaTypedefs.h>
 #include <cuda_runtime.h>
@@ -39,7 +41,8 @@ __device__ __forceinline__ void tc_commit_mc1(uint64_t* bar) {
 
 template <int MODE>
 __global__ void __launch_bounds__(128, 1) mcast_kernel(const __grid_constant__ Maps maps, int iters, int R) {
-  constexpr int S = MODE == 2 ? 3 : 4, kA = (MODE == 2 ? 256 : 128) * 128, kB = 256 * 128, kStage = kA + kB;
+  constexpr int S = MODE == 2 ? 3 : (MODE == 3 ? 6 : 4), kA = (MODE == 2 ? 256 : 128) * 128,
+                kB = (MODE == 3 ? 128 : 256) * 128, kStage = kA + kB;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + S * kStage);
@@ -53,7 +56,10 @@ __global__ void __launch_bounds__(128, 1) mcast_kernel(const __grid_constant__ M
     mbar_init(done, 1);
     fence_barrier_init();
   }
-  if (warp == 1) tmem_alloc<512>(holder);
+  if (warp == 1) {
+    if (MODE == 3) tmem_alloc_pair<512>(holder);
+    else tmem_alloc<512>(holder);
+  }
   tc_fence_before();
   cluster_sync();
   tc_fence_after();
@@ -69,6 +75,14 @@ __global__ void __launch_bounds__(128, 1) mcast_kernel(const __grid_constant__ M
       // (1 MiB each over K = 4096) and 8 B tiles (2 MiB each), 32 MiB in all
       const int arow = ((cluster * 2 + rank) % 16) * 128;
       const int brow = 4096 + (cluster % 8) * 256;
+      if (MODE == 3) {  // both CTAs' loads signal the leader's full barrier
+        const uint32_t fb = smem_addr(&full[ps]) & 0xFEFFFFFFu;
+        if (rank == 0) mbar_arrive_expect_tx(&full[ps], 2 * kStage);
+        tma_load_3d_pair(dst, &maps.a, fb, k0, arow, 0);
+        tma_load_3d_pair(dst + kA, &maps.bh, fb, k0, brow + rank * 128, 0);
+        if (++ps == S) { ps = 0; ph ^= 1; }
+        continue;
+      }
       mbar_arrive_expect_tx(&full[ps], kStage);
       tma_load_3d(dst, &maps.a, &full[ps], k0, arow, 0);
       if (MODE == 2) {
@@ -81,6 +95,23 @@ __global__ void __launch_bounds__(128, 1) mcast_kernel(const __grid_constant__ M
       }
       if (++ps == S) { ps = 0; ph ^= 1; }
     }
+  } else if (warp == 2 && lane == 0 && MODE == 3) {
+    if (rank == 0) {  // the leader issues the pair MMAs
+      int cs = 0, ph = 0;
+      const uint32_t idesc = idesc_bf16_f32(256, 256, 0, 0);
+      for (int it = 0; it < iters; ++it) {
+        mbar_wait(&full[cs], ph);
+        tc_fence_after();
+        const uint32_t la = smem_addr(smem + cs * kStage), ca = la + kA;
+        for (int kk = 0; kk < 4; ++kk)
+          tc_mma_f16_pair(tmem, umma_desc_sw128(la + kk * 32, 16, 1024), umma_desc_sw128(ca + kk * 32, 16, 1024), idesc,
+                          (it | kk) != 0);
+        tc_commit_pair_mc(&empty[cs]);
+        if (++cs == S) { cs = 0; ph ^= 1; }
+      }
+      tc_commit_pair_mc(done);
+    }
+    mbar_wait(done, 0);
   } else if (warp == 2 && lane == 0) {
     int cs = 0, ph = 0;
     const uint32_t idesc = idesc_bf16_f32(128, 256, 0, 0);
@@ -103,7 +134,11 @@ __global__ void __launch_bounds__(128, 1) mcast_kernel(const __grid_constant__ M
   }
   tc_fence_before();
   cluster_sync();
-  if (warp == 1) { tc_fence_after(); tmem_dealloc<512>(tmem); }
+  if (warp == 1) {
+    tc_fence_after();
+    if (MODE == 3) tmem_dealloc_pair<512>(tmem);
+    else tmem_dealloc<512>(tmem);
+  }
 }
 
 // pseudo-random bf16 in [-0.5, 0.5): tensor-core power is data dependent
@@ -143,14 +178,14 @@ int main() {
   make(&m.bh, buf, K, R, 128);
   make(&m.bf, buf, K, R, 256);
   const int ctas = 148, iters = 4096;  // 64 tiles of K=4096 per CTA per launch
-  const int smem = (mode == 2 ? 3 * (256 + 256) : 4 * (128 + 256)) * 128 + 2048;
+  const int smem = (mode == 2 ? 3 * (256 + 256) : (mode == 3 ? 6 * (128 + 128) : 4 * (128 + 256))) * 128 + 2048;
   cudaLaunchConfig_t lc = {};
   lc.gridDim = dim3(ctas); lc.blockDim = dim3(128); lc.dynamicSmemBytes = smem;
   cudaLaunchAttribute at[1];
   at[0].id = cudaLaunchAttributeClusterDimension;
   at[0].val.clusterDim.x = 2; at[0].val.clusterDim.y = 1; at[0].val.clusterDim.z = 1;
   lc.attrs = at; lc.numAttrs = 1;
-  auto kern = mode == 2 ? mcast_kernel<2> : (mode ? mcast_kernel<1> : mcast_kernel<0>);
+  auto kern = mode == 3 ? mcast_kernel<3> : (mode == 2 ? mcast_kernel<2> : (mode ? mcast_kernel<1> : mcast_kernel<0>));
   cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   cudaError_t e = cudaLaunchKernelEx(&lc, kern, m, 64, (int)R);
   cudaDeviceSynchronize();
