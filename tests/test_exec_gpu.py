@@ -320,3 +320,42 @@ def test_eight_warp_epilogue_bitwise_equal(cuda, monkeypatch, case):
         ex.close()
     assert not torch.isnan(outs[0].float()).any()
     assert torch.equal(outs[0], outs[1])
+
+
+@pytest.mark.parametrize("case", ["cluster_splitk", "epi8", "common"])
+def test_graph_replay_matches_eager_bitwise(cuda, case):
+    """CUDA-graph capture and replay (how per-shape timing runs) of each kernel
+    instantiation — on-chip split-K cluster, eight-warp epilogue, the common
+    kernel — writes exactly the eager launch's bits."""
+    from paper_2407_21418_b200.runtime import Planner, bmm_instance, dense_instance
+
+    g = torch.Generator(device="cpu").manual_seed(3)
+    if case == "cluster_splitk":
+        A = (torch.rand(64, 4096, generator=g) * 2 - 1).bfloat16().to(cuda)
+        B = (torch.rand(4096, 4096, generator=g) * 2 - 1).bfloat16().to(cuda)
+        shape, lay, inst = (64, 4096), "nk", dense_instance(64, 4096, 4096)
+    elif case == "epi8":
+        A = (torch.rand(512, 64, 64, generator=g) * 2 - 1).bfloat16().to(cuda)
+        B = (torch.rand(512, 64, 64, generator=g) * 2 - 1).bfloat16().to(cuda)
+        shape, lay, inst = (512, 64, 64), "nk", bmm_instance(512, 64, 64, 64)
+    else:
+        A = (torch.rand(1000, 768, generator=g) * 2 - 1).bfloat16().to(cuda)
+        B = (torch.rand(2304, 768, generator=g) * 2 - 1).bfloat16().to(cuda)
+        shape, lay, inst = (1000, 2304), "nk", dense_instance(1000, 2304, 768)
+    C = torch.full(shape, float("nan"), dtype=torch.bfloat16, device=cuda)
+    ex = Executable([gemm_desc(A, B, C, lay)], [Planner().plan([inst])[0].program], (A, B, C))
+    ex.launch()
+    torch.cuda.synchronize()
+    eager = C.clone()
+    C.fill_(float("nan"))
+    torch.cuda.synchronize()
+    s = torch.cuda.Stream()
+    graph = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(graph, stream=s):
+        ex.launch(s)
+        ex.launch(s)
+    for _ in range(3):
+        graph.replay()
+    torch.cuda.synchronize()
+    assert not torch.isnan(eager.float()).any()
+    assert torch.equal(C, eager)
