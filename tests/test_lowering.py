@@ -104,3 +104,20 @@ def test_output_column_piece_starts_are_tma_aligned(b_layout, orientation, N):
     for _, b, l0, c0, ll, cl, nm, _ in t:
         assert (l0 if swap else c0) % 8 == 0
     assert (apply(t, d, swap) == 1).all()
+
+
+def test_items_rasterised_for_l2_locality():
+    """Each problem's items are ordered by column group (~32 MiB of the column
+    operand over K: 2048 columns at K = 8192), snake order over lanes between
+    groups (exec.cu), and still tile C exactly once."""
+    M = N = K = 8192
+    d = desc(_lib.OP_DENSE, 1, M, N, K, orientation=0)
+    t, _ = lower_table([d], [program_struct(2, 0, [((1, 1), (128, 256, 64), M // 128)])])
+    group = (32 << 20) // (K * 2)
+    gids = [c0 // group for _, _, l0, c0, *_ in t]
+    assert gids == sorted(gids)  # column groups in order
+    for g in sorted(set(gids)):
+        lanes = [l0 for (_, _, l0, c0, *_), gi in zip(t, gids) if gi == g]
+        runs = [lanes[i] for i in range(0, len(lanes), group // 256)]  # one lane value per lane row
+        assert runs == sorted(runs, reverse=(g % 2 == 1))  # snake
+    assert (apply(t, d, False) == 1).all()
