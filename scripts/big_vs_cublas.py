@@ -39,12 +39,14 @@ def run(name, fn, flops, secs=2.0):
     print(f"{name}: {us:.1f} us  {tf:.0f} TF/s  SM {mhz} MHz  -> {tf * 1e12 / (148 * mhz * 1e6):.0f} flop/clk/SM", flush=True)
 
 
-for S in (8192, 4096):
-    A = torch.randn(S, S, device="cuda").bfloat16(); B = torch.randn(S, S, device="cuda").bfloat16()
-    C = torch.empty(S, S, device="cuda", dtype=torch.bfloat16)
-    ex = Executable([gemm_desc(A, B, C, "nk")], [Planner().plan([dense_instance(S, S, S)])[0].program], (A, B, C))
-    fl = 2 * S ** 3
-    run(f"ours   {S}^3", lambda: ex.launch(), fl)
-    run(f"cuBLAS {S}^3", lambda: torch.matmul(A, B.t(), out=C), fl)
-    run(f"ours   {S}^3", lambda: ex.launch(), fl)
+import os
+for spec in os.environ.get("SHAPES", "8192 8192 8192;4096 4096 4096").split(";"):
+    M, N, K = map(int, spec.split())
+    A = torch.randn(M, K, device="cuda").bfloat16(); B = torch.randn(N, K, device="cuda").bfloat16()
+    C = torch.empty(M, N, device="cuda", dtype=torch.bfloat16)
+    ex = Executable([gemm_desc(A, B, C, "nk")], [Planner().plan([dense_instance(M, N, K)])[0].program], (A, B, C))
+    fl = 2 * M * N * K
+    run(f"ours   {M}x{N}x{K}", lambda: ex.launch(), fl)
+    run(f"cuBLAS {M}x{N}x{K}", lambda: torch.matmul(A, B.t(), out=C), fl)
+    run(f"ours   {M}x{N}x{K}", lambda: ex.launch(), fl)
     ex.close()
