@@ -6,6 +6,7 @@ import pytest
 
 ROOT = Path(__file__).resolve().parents[1]
 sys.path.insert(0, str(ROOT))
+sys.path.insert(0, str(ROOT / "tests" / "golden"))  # cases.py: workload documents shared with make_golden.py
 os.environ.setdefault("PYTHONDONTWRITEBYTECODE", "1")
 
 REFERENCE_SRC = Path("/root/reference/pkg/src")

@@ -61,3 +61,26 @@ def test_missing_metrics():
     k = ukernel.UKernel(reg_tile={"i": 1, "j": 1}, smem_tile={"i": 7, "j": 64, "k": 64})
     with pytest.raises(errors.MissingMetricsError):
         scoring.rank_topk([k], inst)
+
+
+def test_missing_library_fails_loudly(tmp_path):
+    """No CPU fallback: with libftb.so absent, planning (and therefore every
+    execute path) raises LibraryMissing instead of routing anywhere else."""
+    import os
+    import subprocess
+    import sys
+
+    code = (
+        "from paper_2407_21418_b200 import _lib\n"
+        "from paper_2407_21418_b200.runtime import Planner, dense_instance\n"
+        "try:\n"
+        "    Planner().plan([dense_instance(128, 768, 768)])\n"
+        "except _lib.LibraryMissing as e:\n"
+        "    print('RAISED', e)\n"
+        "else:\n"
+        "    print('NO-RAISE')\n"
+    )
+    env = dict(os.environ, FTB_LIB=str(tmp_path / "absent_libftb.so"))
+    out = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True, timeout=300,
+                         cwd=os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+    assert "RAISED" in out.stdout, out.stdout + out.stderr
