@@ -157,17 +157,7 @@ def check(status: int) -> None:
     from .mktune import errors as E
 
     msg, field = last_error()
-    if status == FTB_INPUT_ERROR:
-        raise E.InputError(msg, field=field or None)
-    if status == FTB_EMPTY_RESULT:
-        raise E.EmptyResultError(msg, constraint=field or None)
-    if status == FTB_CAPACITY_ERROR:
-        raise E.CapacityError(msg)
-    if status == FTB_MISSING_METRICS:
-        raise E.MissingMetricsError(msg)
-    if status == FTB_CUDA_ERROR:
-        raise E.DeviceError(msg)
-    raise E.InternalError(msg)
+    raise E.TunerError.from_status(status, msg, field)
 
 
 def env_flag(name: str) -> bool:
