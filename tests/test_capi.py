@@ -84,3 +84,26 @@ def test_missing_library_fails_loudly(tmp_path):
     out = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True, timeout=300,
                          cwd=os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
     assert "RAISED" in out.stdout, out.stdout + out.stderr
+
+
+def test_status_codes_map_onto_error_classes():
+    """Each FTB_* status of include/ftb.h becomes its mktune.errors class
+    (errors.py:10-47), with the CLI exit code the reference assigns."""
+    from paper_2407_21418_b200.mktune import errors as E
+
+    cases = {
+        _lib.FTB_INPUT_ERROR: (E.InputError, 2),
+        _lib.FTB_EMPTY_RESULT: (E.EmptyResultError, 1),
+        _lib.FTB_INTERNAL_ERROR: (E.InternalError, 3),
+        _lib.FTB_CAPACITY_ERROR: (E.CapacityError, 2),
+        _lib.FTB_MISSING_METRICS: (E.MissingMetricsError, 3),
+        _lib.FTB_CUDA_ERROR: (E.DeviceError, 3),
+    }
+    for status, (cls, exit_code) in cases.items():
+        e = E.TunerError.from_status(status, "msg", "fld")
+        assert type(e) is cls and e.exit_code == exit_code and str(e) == "msg"
+    assert E.TunerError.from_status(_lib.FTB_INPUT_ERROR, "m", "fld").field == "fld"
+    assert E.TunerError.from_status(_lib.FTB_EMPTY_RESULT, "m", "c").constraint == "c"
+    assert E.InputError("m", "f").field == "f" and E.EmptyResultError("m", "c", "h").hint == "h"
+    with pytest.raises(TypeError):
+        E.InputError("m", "f", "extra")
