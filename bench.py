@@ -1,17 +1,23 @@
 #!/usr/bin/env python3
 """Benchmark: dynamic-shape Dense+BMM over the C1 shape set (BERT-base,
-batch 32, GLUE-like sequence lengths), executed as mixed-size uKernels by one
-persistent sm_100a launch per step.
+batch 32, GLUE-like sequence lengths), each GEMM executed as a patchwork of
+mixed-size uKernels by the persistent sm_100a kernel.
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+Headline (BASELINE.json metric "dynamic-shape GEMM TFLOP/s (shape-set mean)
+vs roofline"): every shape is its own launch, timed L2-cold (its launches
+cycle over >= 252 MB of operand copies); value = mean over shapes of the
+per-shape TFLOP/s, with the per-shape roofline fractions beside it. The whole
+set as ONE grouped launch is reported as `grouped_step`; `e2e` is the same
+shape-set mean through the public API with host buffers; the reference arm
+(--impl reference) runs the oracle's numpy fp32 restatement of the same 192
+shapes on the host cores.
 
 One process per GPU (torchrun for N>1). Each rank draws its own sequence
 lengths (seed = rank), so per-GPU work is fixed as N grows ("weak"); there is
 no collective on the data path — ranks only meet at the timing barriers and
-the final max-over-ranks reduction. Rank 0 prints ONE JSON line.
-
-A "step" = one pass of the hot path over the whole shape set: every Dense
-and BMM of every sequence length, executed from the lowered tile table.
+the final max / sum over ranks. Rank 0 prints ONE JSON line.
 """
 
 from __future__ import annotations
@@ -148,34 +154,42 @@ def sum_over_ranks(x: float, world: int) -> float:
 # ----------------------------------------------------------------------------- cpu baseline
 
 
-def cpu_execute_sample(shapes, seconds_budget: float = 20.0, min_seconds: float = 0.0) -> dict:
+def cpu_shape_set(shapes, passes: int = 1, seconds_budget: float = 60.0) -> dict:
     """ORACLE leg (bench.py cpu_baseline / --impl reference only): the numpy
-    fp32 restatement of plan execution (oracle/execute_np.py) over the shape
-    set, on all host cores. Passes over the set repeat until min_seconds of
-    compute have accumulated; a pass stops early past seconds_budget."""
+    fp32 restatement of executing each shape (oracle/execute_np.py) on all
+    host cores, shape by shape like the GPU arm's per-shape launches. Returns
+    the shape-set mean TFLOP/s (mean over shapes of F / t) and the aggregate."""
     import numpy as np
 
     from oracle.execute_np import execute_dense_fp32
 
     rng = np.random.default_rng(0)
-    flops = 0
-    t_total = 0.0
-    done = 0
+    per = {}
     t_start = time.perf_counter()
-    while True:
-        for s in shapes:
+    for _ in range(passes):
+        for i, s in enumerate(shapes):
             A = rng.uniform(-1, 1, (s.batch, s.M, s.K)).astype(np.float32)
             B = rng.uniform(-1, 1, (s.batch if s.kind == "bmm" else 1, s.K, s.N)).astype(np.float32)
             t0 = time.perf_counter()
             execute_dense_fp32(A, B)
-            t_total += time.perf_counter() - t0
-            flops += s.flops
-            done += 1
+            per.setdefault(i, []).append(time.perf_counter() - t0)
             if time.perf_counter() - t_start > seconds_budget:
                 break
-        if t_total >= min_seconds or time.perf_counter() - t_start > seconds_budget:
-            break
-    return {"tflops": flops / t_total / 1e12, "shapes": done, "seconds": t_total}
+    done = sorted(per)
+    ts = {i: statistics.median(per[i]) for i in done}
+    mean = sum(shapes[i].flops / ts[i] for i in done) / len(done) / 1e12
+    agg = sum(shapes[i].flops for i in done) / sum(ts.values()) / 1e12
+    return {"mean_tflops": mean, "agg_tflops": agg, "shapes": len(done), "passes": passes,
+            "seconds": sum(sum(v) for v in per.values()), "ms_per_pass": 1e3 * sum(ts.values())}
+
+
+def bench_shapes(args, seed: int):
+    from paper_2407_21418_b200.workloads import c1_shapes
+
+    shapes = c1_shapes(n_draws=args.draws, seed=seed)
+    if args.ops != "all":
+        shapes = [s for s in shapes if s.kind == args.ops]
+    return shapes
 
 
 # ----------------------------------------------------------------------------- arms
@@ -183,47 +197,180 @@ def cpu_execute_sample(shapes, seconds_budget: float = 20.0, min_seconds: float 
 
 def run_reference(args, rank, world):
     """--impl reference: the reference's CPU path restated by the oracle
-    (numpy fp32 execute of the same shape set) on the host cores."""
+    (numpy fp32 execute of the SAME 192-shape set, shape by shape) on all
+    host cores; value = the same shape-set-mean TFLOP/s metric."""
     if rank != 0:
         return
-    from paper_2407_21418_b200.workloads import c1_shapes
-
-    shapes = c1_shapes(n_draws=args.draws, seed=0)
-    sample = [s for s in shapes][: 6 * 8]  # the 8 canonical sequence lengths (48 GEMMs)
+    shapes = bench_shapes(args, seed=0)
     cores = os.cpu_count()
-    for _ in range(args.warmup):
-        cpu_execute_sample(sample[:6], 5.0)
-    vals = []
+    cpu_shape_set(shapes[:6], passes=max(1, args.warmup // 3))
     t_all = time.perf_counter()
-    for _ in range(args.steps):
-        vals.append(cpu_execute_sample(sample, 60.0))
+    r = cpu_shape_set(shapes, passes=args.steps, seconds_budget=240.0)
     wall = time.perf_counter() - t_all
-    flops = sum(v["tflops"] * v["seconds"] * 1e12 for v in vals)
-    secs = sum(v["seconds"] for v in vals)
-    value = flops / secs / 1e12
     line = {
-        "impl": "reference", "metric": METRIC, "value": value, "unit": "TFLOP/s", "n_gpus": args.gpus,
-        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * secs / max(1, args.steps),
+        "impl": "reference", "metric": METRIC, "value": r["mean_tflops"], "unit": "TFLOP/s", "n_gpus": args.gpus,
+        "steps": r["passes"], "warmup": args.warmup, "ms_per_step": r["ms_per_pass"],
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
-        "config": {"workload": WORKLOAD, "sample": "8 canonical T x 6 GEMMs (48 shapes) per step",
+        "config": {"workload": WORKLOAD, "n_shapes": len(shapes), "shapes_timed": r["shapes"],
+                   "step": "one pass over the shape set, one numpy matmul per shape (median over passes)",
                    "parallelism": "cpu"},
-        "cpu_baseline": {"value": value, "unit": "TFLOP/s", "cores": cores, "kind": "port",
-                         "sample": "numpy fp32 A@B (OpenBLAS, all cores) over 48 C1 GEMMs per step"},
-        "e2e": {"value": value, "unit": "TFLOP/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "aggregate_tflops": r["agg_tflops"],
+        "cpu_baseline": {"value": r["mean_tflops"], "unit": "TFLOP/s", "cores": cores, "kind": "port",
+                         "sample": f"numpy fp32 A@B (oracle/execute_np.py, OpenBLAS on all cores) per shape over "
+                                   f"the same {len(shapes)}-shape C1 set as the GPU arm, {r['passes']} passes"},
+        "e2e": {"value": r["mean_tflops"], "unit": "TFLOP/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
         "wall_s": wall,
     }
     print(json.dumps(line), flush=True)
 
 
+def lib_sha() -> str:
+    import hashlib
+
+    p = ROOT / "paper_2407_21418_b200" / "libftb.so"
+    return hashlib.sha256(p.read_bytes()).hexdigest()[:16] if p.exists() else ""
+
+
 def load_traffic(tag: str):
+    """Per-launch DRAM bytes of the dominant kernel from the ncu artefact
+    (scripts/ncu_traffic.py), used only when it was measured on THIS build
+    of libftb.so (sha256 prefix) — otherwise null with the reason."""
     p = ROOT / "profiles" / "ncu_traffic.json"
     if not p.exists():
-        return None
+        return None, "no ncu artefact"
     try:
-        d = json.loads(p.read_text())
-        return d.get(tag)
+        d = json.loads(p.read_text()).get(tag)
     except json.JSONDecodeError:
-        return None
+        return None, "unreadable ncu artefact"
+    if not isinstance(d, dict):
+        return None, f"no per-build '{tag}' entry in the ncu artefact"
+    if d.get("lib_sha") != lib_sha():
+        return None, f"ncu artefact is for libftb.so {d.get('lib_sha')}, this build is {lib_sha()}"
+    return d.get("dram_bytes_per_launch"), "ncu dram__bytes_read.sum + dram__bytes_write.sum, " + d.get("how", "")
+
+
+def _copy_like(view, store):
+    """A fresh buffer with `store`'s layout and the view of it `view` is."""
+    import torch
+
+    new = torch.empty_like(store)
+    new.copy_(store)
+    return new, new.as_strided(view.size(), view.stride())
+
+
+def per_shape_timing(ss, P, dev, reps: int, l2_bytes: float, max_copies: int = 1024):
+    """Each shape as its own launch (its own single-problem table), inputs
+    L2-cold: the launches of shape s cycle over R_s copies of its operands
+    and output with R_s * bytes_s >= l2_bytes (2x the 126 MB L2), so every
+    launch reads operands last touched >= 252 MB of traffic earlier. The
+    L_s = max(R_s, 20) launches are PDL-chained in a CUDA graph (consecutive
+    GEMMs on different buffers, as in a model); per-launch time = replay
+    time / L_s, the median over `reps` timed replays."""
+    import math
+
+    import torch
+
+    from paper_2407_21418_b200.execute import Executable, gemm_desc
+
+    s = torch.cuda.Stream(dev)
+    rows, launches, exes_made = [], 0, 0
+    for x, rec in zip(ss.bound, ss.records):
+        sh = x.shape
+        R = max(1, min(max_copies, math.ceil(l2_bytes / max(1, sh.bytes))))
+        L = max(R, 20)
+        exes, keep = [], []
+        for r in range(R):
+            if r == 0:
+                A, B, C = x.A, x.B, x.C
+            else:
+                _, A = _copy_like(x.A, x.A_store)
+                B = x.B.clone()
+                _, C = _copy_like(x.C, x.C_store)
+            keep.append((A, B, C))
+            exes.append(Executable([gemm_desc(A, B, C, sh.b_layout)], [rec.program]))
+        exes_made += R
+        with torch.cuda.stream(s):
+            for e in exes:
+                e.launch(s)
+        torch.cuda.synchronize(dev)
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g, stream=s):
+            for i in range(L):
+                exes[i % R].launch(s)
+        with torch.cuda.stream(s):
+            g.replay()
+        torch.cuda.synchronize(dev)
+        ts = []
+        for _ in range(reps):
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            with torch.cuda.stream(s):
+                e0.record(s)
+                g.replay()
+                e1.record(s)
+            torch.cuda.synchronize(dev)
+            ts.append(e0.elapsed_time(e1) * 1e-3 / L)
+        launches += reps * L
+        t = statistics.median(ts)
+        rows.append({"name": sh.name, "b": sh.batch, "M": sh.M, "N": sh.N, "K": sh.K, "us": t * 1e6,
+                     "tflops": sh.flops / t / 1e12, "frac": sh.t_roof(P) / t,
+                     "frac_measured_hbm": max(sh.flops / P, sh.bytes / ss.hbm_bps) / t, "bound": sh.bound(P),
+                     "copies": R, "launches_per_replay": L})
+        del g, exes, keep
+    fr = sorted(r["frac"] for r in rows)
+    kinds = sorted({r["name"] for r in rows})
+    return {
+        "rows": rows, "mean_frac": sum(fr) / len(fr), "p10_frac": fr[int(0.1 * (len(fr) - 1))],
+        "median_frac": statistics.median(fr),
+        "mean_frac_measured_hbm": sum(r["frac_measured_hbm"] for r in rows) / len(rows),
+        "mean_tflops": sum(r["tflops"] for r in rows) / len(rows),
+        "by_kind": {k: sum(r["frac"] for r in rows if r["name"] == k) / sum(1 for r in rows if r["name"] == k)
+                    for k in kinds},
+        "sum_us": sum(r["us"] for r in rows), "launches": launches, "tables": exes_made,
+    }
+
+
+def e2e_per_shape(ss, planner, dev, passes: int):
+    """The same shape-set-mean metric end to end through the public API
+    (Planner.dense / Planner.bmm — plan-cache lookup, table cache, launch),
+    every shape in turn: its activations H2D from pinned host memory, the
+    GEMM, its output D2H to pinned host memory, all inside the per-shape
+    CUDA-event window on one stream (weights stay resident). One pass walks
+    all shapes, so each shape's weights are L2-cold (>= 2 GB of traffic
+    between its turns). Per-shape time = median over passes."""
+    import torch
+
+    s = torch.cuda.current_stream(dev)
+    host_in = [[t.cpu().pin_memory() for t in x.inputs] for x in ss.bound]
+    host_out = [x.C.cpu().pin_memory() for x in ss.bound]
+    per = [[] for _ in ss.bound]
+
+    def one(i, x, timed):
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(s)
+        for dst, src in zip(x.inputs, host_in[i]):
+            dst.copy_(src, non_blocking=True)
+        sh = x.shape
+        if sh.kind == "dense":
+            planner.dense(x.A, x.B, b_layout=sh.b_layout, out=x.C, stream=s)
+        else:
+            planner.bmm(x.A, x.B, b_layout=sh.b_layout, dynamic=sh.dynamic, out=x.C, stream=s)
+        host_out[i].copy_(x.C, non_blocking=True)
+        e1.record(s)
+        return (e0, e1) if timed else None
+
+    for i, x in enumerate(ss.bound):  # warm the plan and table caches
+        one(i, x, False)
+    torch.cuda.synchronize(dev)
+    for _ in range(passes):
+        evs = [one(i, x, True) for i, x in enumerate(ss.bound)]
+        torch.cuda.synchronize(dev)
+        for i, (e0, e1) in enumerate(evs):
+            per[i].append(e0.elapsed_time(e1) * 1e-3)
+    ts = [statistics.median(p) for p in per]
+    h2d = sum(t.numel() * t.element_size() for x in ss.bound for t in x.inputs)
+    d2h = sum(x.C.numel() * x.C.element_size() for x in ss.bound)
+    return {"mean_tflops": sum(x.shape.flops / t for x, t in zip(ss.bound, ts)) / len(ts) / 1e12,
+            "ms_per_pass": 1e3 * sum(ts), "h2d": h2d, "d2h": d2h}
 
 
 def run_ours(args, rank, world, local):
@@ -231,23 +378,32 @@ def run_ours(args, rank, world, local):
 
     from paper_2407_21418_b200.runtime import Planner
     from paper_2407_21418_b200.shapeset import ShapeSet
-    from paper_2407_21418_b200.workloads import c1_shapes
 
     dev = torch.device("cuda", local)
     torch.cuda.set_device(dev)
     peaks = measured_peaks()
     P = peaks["bf16_tflops"] * 1e12
-    shapes = c1_shapes(n_draws=args.draws, seed=rank)
-    if args.ops != "all":
-        shapes = [s for s in shapes if s.kind == args.ops]
+    shapes = bench_shapes(args, seed=rank)
     planner = Planner()
     ss = ShapeSet(shapes, planner, device=dev, seed=rank, pinned=True)
-    ss._make_twin()
+    ss.hbm_bps = peaks["hbm_gbs"] * 1e9
     stream = torch.cuda.current_stream(dev)
     info = ss.exe.info
 
-    # ------------------------------------------------ device-resident timing
     clocks = ClockSampler(local).start()
+    # ------------------------------------------------ headline: per-shape launches, L2-cold
+    barrier(world)
+    torch.cuda.synchronize(dev)
+    t_wall0 = time.perf_counter()
+    ps = per_shape_timing(ss, P, dev, reps=args.steps, l2_bytes=2 * 126e6)
+    torch.cuda.synchronize(dev)
+    barrier(world)
+    ps_wall = time.perf_counter() - t_wall0
+    mean_rank = ps["mean_tflops"]
+    value = sum_over_ranks(mean_rank, world)  # N GPUs run their shape sets concurrently
+    step_ms = max_over_ranks(ps["sum_us"] * 1e-3, world)
+
+    # ------------------------------------------------ grouped step: all shapes in ONE launch
     t_end = time.perf_counter() + args.min_warm_s
     w = 0
     while w < args.warmup or time.perf_counter() < t_end:
@@ -265,143 +421,101 @@ def run_ours(args, rank, world, local):
         e1.record(stream)
     torch.cuda.synchronize(dev)
     barrier(world)
-    per_launch = [e0.elapsed_time(e1) for e0, e1 in ev]  # ms, on the launching stream
     clk = clocks.stop()
-    t_step_ms = sum(per_launch) / len(per_launch)
-    t_max_ms = max_over_ranks(t_step_ms, world)
-
-    # ------------------------------------------------ end-to-end (host buffers)
-    # every step: all inputs H2D from pinned host memory, one launch, all
-    # outputs D2H; copies of neighbouring steps overlap the launch (two device
-    # buffer sets, full-duplex copy streams)
-    ss.e2e_pipelined(2, stream)
-    barrier(world)
-    # 30 steps (~0.5 s): the pipeline's fill (first H2D alone) and drain (last
-    # D2H alone) cost ~15 ms once, so a short window understates the sustained
-    # rate by (fill + drain) / steps
-    e2e_steps = 30
-    e2e_ms = max_over_ranks(ss.e2e_pipelined(e2e_steps, stream), world)
-
-    # ------------------------------------------------ per-shape roofline fractions
-    # (one launch per shape, back to back in a CUDA graph; shape-set mean)
-    shape_fracs = None
-    if args.per_shape and world == 1:
-        shape_fracs = per_shape_fracs(ss, planner, P, dev)
-
+    per_launch = [e0.elapsed_time(e1) for e0, e1 in ev]
+    t_step_ms = max_over_ranks(sum(per_launch) / len(per_launch), world)
     flops_rank = ss.true_flops
-    flops_all = sum_over_ranks(float(flops_rank), world)
     bytes_rank = ss.alg_bytes
-    value = flops_all / (t_max_ms * 1e-3) / 1e12
-    e2e_value = flops_all / (e2e_ms * 1e-3) / 1e12
-    t_roof_sum = sum(s.t_roof(P) for s in ss.shapes)
-    # dominant kernel = the single persistent launch of the step
-    t_tc = flops_rank / P
-    t_hbm = bytes_rank / (peaks["hbm_gbs"] * 1e9)
-    bound = "tensor" if t_tc >= t_hbm else "hbm"
-    if bound == "tensor":
-        achieved = flops_rank / (t_step_ms * 1e-3) / 1e12
-        # the timed region is a long, power-capped run (>= 1 s of back-to-back
-        # steps): its denominator is the sustained cuBLAS figure; the burst
-        # figure is reported beside it
-        sus = peaks.get("bf16_tflops_sustained") or peaks["bf16_tflops"]
-        roof = {"bound": "tensor", "achieved": achieved, "peak": sus, "unit": "TFLOP/s",
-                "frac": achieved / sus, "peak_burst": peaks["bf16_tflops"],
-                "frac_of_burst": achieved / peaks["bf16_tflops"]}
-    else:
-        achieved = bytes_rank / (t_step_ms * 1e-3) / 1e9
-        roof = {"bound": "hbm", "achieved": achieved, "peak": peaks["hbm_gbs"], "unit": "GB/s",
-                "frac": achieved / peaks["hbm_gbs"]}
-    roof["traffic"] = load_traffic("c1_step")
-    roof["peak_source"] = (peaks["source"] + (" (MEASURED_PEAKS.json: sustained for tensor-bound, hbm_gbs for hbm-bound)"
-                                              if peaks["source"] == "measured" else ""))
-    roof["algorithmic_flops_per_launch"] = flops_rank
-    roof["algorithmic_bytes_per_launch"] = bytes_rank
+    sus = peaks.get("bf16_tflops_sustained") or peaks["bf16_tflops"]
+    g_ach = flops_rank / (t_step_ms * 1e-3) / 1e12
+    traffic_g, traffic_g_how = load_traffic("c1_step")
+    grouped = {
+        "ms_per_step": t_step_ms, "tflops": sum_over_ranks(g_ach, world), "launches": args.steps,
+        "warmup_launches": w, "work_items": info.n_work, "ctas": info.n_ctas,
+        "roofline": {"bound": "tensor" if flops_rank / P >= bytes_rank / (peaks["hbm_gbs"] * 1e9) else "hbm",
+                     "achieved": g_ach, "peak": sus, "unit": "TFLOP/s", "frac": g_ach / sus,
+                     "peak_source": "MEASURED_PEAKS bf16_tflops_sustained (a >= 1 s power-capped run)",
+                     "peak_burst": peaks["bf16_tflops"], "frac_of_burst": g_ach / peaks["bf16_tflops"],
+                     "traffic": traffic_g, "traffic_source": traffic_g_how,
+                     "algorithmic_flops_per_launch": flops_rank, "algorithmic_bytes_per_launch": bytes_rank},
+        "roofline_sum_of_shapes_frac": sum(s.t_roof(P) for s in ss.shapes) * 1e3 / t_step_ms,
+        "l2": f"no flush: step footprint {bytes_rank / 1e9:.2f} GB > 126 MB L2",
+    }
+
+    # ------------------------------------------------ end to end through the public API
+    e2e = e2e_per_shape(ss, planner, dev, passes=max(3, args.steps // 4))
+    e2e_value = sum_over_ranks(e2e["mean_tflops"], world)
+
+    # ------------------------------------------------ roofline of the headline launches
+    sum_t = ps["sum_us"] * 1e-6
+    ach = flops_rank / sum_t / 1e12
+    traffic, traffic_how = load_traffic("c1_per_shape")
+    roof = {"bound": "tensor", "achieved": ach, "peak": peaks["bf16_tflops"], "unit": "TFLOP/s",
+            "frac": ach / peaks["bf16_tflops"],
+            "peak_source": peaks["source"] + " MEASURED_PEAKS bf16_tflops (burst: each shape is timed alone)",
+            "achieved_def": "sum of the set's FLOPs / sum of its per-shape launch times (one launch per shape)",
+            "set_roofline_frac": sum(s.t_roof(P) for s in ss.shapes) / sum_t,
+            "traffic": traffic, "traffic_source": traffic_how,
+            "algorithmic_flops_per_launch_set": flops_rank, "algorithmic_bytes_per_launch_set": bytes_rank}
 
     line = {
         "metric": METRIC, "value": value, "unit": "TFLOP/s", "n_gpus": world, "steps": args.steps,
-        "warmup": args.warmup, "warmup_launches": w, "ms_per_step": t_max_ms, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
-        "dtype": "bf16", "data": "synthetic (U(-1,1) bf16 activations and weights, seeded per rank)",
+        "warmup": args.warmup, "ms_per_step": step_ms, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "bf16",
+        "data": "synthetic (U(-1,1) bf16 activations and weights, seeded per rank)",
         "config": {
-            "workload": WORKLOAD, "n_shapes_per_gpu": len(shapes), "shapes_per_step": len(shapes),
+            "workload": WORKLOAD, "n_shapes_per_gpu": len(shapes),
+            "value_def": "shape-set mean of per-shape TFLOP/s (true FLOPs / per-launch time), each shape its own "
+                         "launch; summed over ranks at N > 1",
+            "step": "every shape once, one launch per shape (ms_per_step = sum of per-shape launch times); each "
+                    "shape timed as the median of `steps` CUDA-graph replays of its L2-cold launch chain",
             "parallelism": f"shape-sharded x{world} (no data-path collective)",
-            "l2": f"no flush: step footprint {(ss.alg_bytes) / 1e9:.2f} GB > 126 MB L2",
+            "l2": "inputs larger than L2: each shape's launches cycle over copies of its operands totalling "
+                  ">= 252 MB (2x L2), so no launch finds its operands in L2",
         },
         "roofline": roof,
-        "roofline_sum_of_shapes": {"t_roof_ms": t_roof_sum * 1e3, "frac_of_step": t_roof_sum * 1e3 / t_step_ms},
-        "shape_set_mean_roofline_frac": None if shape_fracs is None else shape_fracs["mean_frac"],
-        "shape_set_mean_tflops": None if shape_fracs is None else shape_fracs["mean_tflops"],
+        "shape_set_mean_roofline_frac": ps["mean_frac"],
+        "shape_set_p10_roofline_frac": ps["p10_frac"],
+        "shape_set_median_roofline_frac": ps["median_frac"],
+        "shape_set_roofline_def": "t_roof = max(F / bf16_tflops (MEASURED_PEAKS burst), bytes / 8 TB/s (north_star "
+                                  "HBM figure)); frac = t_roof / t_measured; mean over shapes",
+        "shape_set_mean_roofline_frac_measured_hbm": ps["mean_frac_measured_hbm"],
+        "shape_set_frac_by_kind": ps["by_kind"],
         "tuning_s": ss.tuning_s,
         "tuning_s_per_shape": ss.tuning_s / len(shapes),
         "padding_pct": 100.0 * ss.padding_ratio(),
         "mma_padding_pct": 100.0 * (1 - info.true_flops / info.mma_flops) if info.mma_flops else None,
-        "e2e": {"value": e2e_value, "unit": "TFLOP/s", "h2d_bytes_per_step": ss.h2d_bytes,
-                "d2h_bytes_per_step": ss.d2h_bytes, "ms_per_step": e2e_ms, "steps": e2e_steps,
-                "mode": "every step moves all inputs H2D and all outputs D2H (pinned); copies of steps k-1/k+1 "
-                        "overlap step k's launch (two device buffer sets, separate H2D/D2H streams)"},
-        "gpu_launches": args.steps,
-        "work_items": info.n_work, "ctas": info.n_ctas,
+        "grouped_step": grouped,
+        "e2e": {"value": e2e_value, "unit": "TFLOP/s", "h2d_bytes_per_step": e2e["h2d"],
+                "d2h_bytes_per_step": e2e["d2h"], "ms_per_step": e2e["ms_per_pass"],
+                "mode": "shape-set mean through Planner.dense/bmm: per shape, activations H2D from pinned host "
+                        "memory + launch + output D2H to pinned memory inside its event window (weights resident)"},
+        "gpu_launches": ps["launches"] + args.steps,
+        "gpu_launches_def": "per-shape timed launches (sum over shapes of steps x chain length) + grouped steps",
+        "per_shape_tables": ps["tables"],
+        "per_shape_wall_s": ps_wall,
         "clocks": clk,
     }
     if rank == 0 and world == 1 and not args.no_cpu:
-        cb = cpu_execute_sample(list(shapes), seconds_budget=40.0, min_seconds=10.0)
-        line["cpu_baseline"] = {"value": cb["tflops"], "unit": "TFLOP/s", "cores": os.cpu_count(), "kind": "port",
-                                "sample": f"numpy fp32 A@B (oracle/execute_np.py) over {cb['shapes']} C1 GEMMs "
-                                          f"(passes over this rank's shape set), {cb['seconds']:.1f} s of compute, "
-                                          f"OpenBLAS on all cores"}
-    if shape_fracs is not None:
-        line["per_shape"] = shape_fracs["rows"] if args.per_shape_rows else None
+        cb = cpu_shape_set(list(shapes), passes=2, seconds_budget=30.0)
+        line["cpu_baseline"] = {"value": cb["mean_tflops"], "unit": "TFLOP/s", "cores": os.cpu_count(),
+                                "kind": "port", "aggregate_tflops": cb["agg_tflops"],
+                                "sample": f"numpy fp32 A@B per shape (oracle/execute_np.py, OpenBLAS on all cores) "
+                                          f"over the same {cb['shapes']}-shape set, {cb['passes']} passes, "
+                                          f"{cb['seconds']:.1f} s of compute"}
+    line["per_shape"] = ps["rows"] if args.per_shape_rows else None
     if rank == 0:
         print(json.dumps(line), flush=True)
-
-
-def per_shape_fracs(ss, planner, P, dev):
-    """Each shape as its own launch (its own single-problem table), timed
-    back to back inside a CUDA graph; fraction = t_roof / t_measured."""
-    import torch
-
-    from paper_2407_21418_b200.execute import Executable, gemm_desc
-
-    rows = []
-    exes = []
-    for x, rec in zip(ss.bound, ss.records):
-        exes.append(Executable([gemm_desc(x.A, x.B, x.C, x.shape.b_layout)], [rec.program], (x.A, x.B, x.C)))
-    s = torch.cuda.Stream(dev)
-    reps = 20
-    with torch.cuda.stream(s):
-        for e in exes:
-            e.launch(s)
-    torch.cuda.synchronize(dev)
-    for e, x in zip(exes, ss.bound):
-        g = torch.cuda.CUDAGraph()
-        with torch.cuda.graph(g, stream=s):
-            for _ in range(reps):
-                e.launch(s)
-        with torch.cuda.stream(s):
-            g.replay()
-        torch.cuda.synchronize(dev)
-        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        with torch.cuda.stream(s):
-            e0.record(s)
-            g.replay()
-            e1.record(s)
-        torch.cuda.synchronize(dev)
-        t = e0.elapsed_time(e1) / reps * 1e-3
-        sh = x.shape
-        rows.append({"name": sh.name, "b": sh.batch, "M": sh.M, "N": sh.N, "K": sh.K, "us": t * 1e6,
-                     "tflops": sh.flops / t / 1e12, "frac": sh.t_roof(P) / t, "bound": sh.bound(P)})
-    return {"rows": rows, "mean_frac": sum(r["frac"] for r in rows) / len(rows),
-            "mean_tflops": sum(r["tflops"] for r in rows) / len(rows)}
 
 
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=50)
+    ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=10)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--draws", type=int, default=24)
     ap.add_argument("--min-warm-s", type=float, default=1.0)
-    ap.add_argument("--per-shape", type=int, default=1)
     ap.add_argument("--per-shape-rows", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--ops", choices=["all", "dense", "bmm"], default="all")

@@ -216,7 +216,7 @@ def cmd_plan(args) -> int:
     cache = json.loads(Path(args.cache).read_text()) if args.cache else None
     if args.cache and cache.get("kind") != "candidate-cache":
         raise E.InputError(f"{args.cache} is not a candidate cache", field="cache")
-    shapes = []
+    shapes, timings = [], []
     for b in _bindings(spec, args.shape, args.range):
         inst = WorkloadInstance(spec=spec, bindings=b)
         cands = _candidates_from_cache(cache, spec, hw, b) if cache else None
@@ -228,17 +228,41 @@ def cmd_plan(args) -> int:
         top = rank_topk(cands, inst, coeffs=coeffs, k=args.topk)
         t2 = time.perf_counter()
         shapes.append({"binding": b, "extents": inst.extents, "candidates": len(cands), "source": source,
-                       "tau": select_main_axis(inst), "plans": [_plan_doc(p, inst, hw, coeffs) for p in top],
-                       "timing": {"compile_s": t1 - t0, "combine_rank_s": t2 - t1}})
+                       "tau": select_main_axis(inst), "plans": [_plan_doc(p, inst, hw, coeffs) for p in top]})
+        timings.append({"binding": b, "compile_s": t1 - t0, "combine_rank_s": t2 - t1})
     doc = dict(_provenance(spec, hw), kind="plan-report", coeffs=coeffs.to_doc(), topk=args.topk,
                axes={"space": list(spec.space_axes), "reduce": list(spec.reduce_axes)},
                inputs=[[a.tensor, list(a.axes)] for a in spec.input_accesses],
                output=[spec.output_access.tensor, list(spec.output_access.axes)], shapes=shapes)
+    # The plan report is deterministic (SPEC "All commands are deterministic");
+    # the wall-clock of combine + rank (SPEC cmd_plan: "recorded in the
+    # report") goes to a separate timing report when --timings PATH is given.
+    if args.timings:
+        Path(args.timings).write_text(json.dumps(dict(_provenance(spec, hw), kind="plan-timings", shapes=timings),
+                                                 sort_keys=True, indent=1) + "\n")
     if args.emit == "loopnest":
         _write(loopnest_text(doc, args.index), args.out)
+    elif args.emit == "csv":
+        _write(plan_csv(doc), args.out)
     else:
         _write(json.dumps(doc, sort_keys=True, indent=1) + "\n", args.out)
     return 0
+
+
+def plan_csv(doc: dict) -> str:
+    """One CSV row per (shape, ranked plan) of a plan report (SPEC --emit csv)."""
+    cols = ["schema", "descriptor", "workload_hash", "binding", "rank", "tau", "parts", "sia", "est_total_s",
+            "padding_fraction"]
+    buf = io.StringIO()
+    w = csv.DictWriter(buf, fieldnames=cols, lineterminator="\n")
+    w.writeheader()
+    for sh in doc["shapes"]:
+        for r, p in enumerate(sh["plans"]):
+            w.writerow({"schema": SCHEMA, "descriptor": doc["descriptor"], "workload_hash": doc["workload_hash"],
+                        "binding": _binding_key(sh["binding"]), "rank": r, "tau": p["tau"],
+                        "parts": " + ".join(f"{q['count']}x{q['smem']}" for q in p["parts"]), "sia": repr(p["sia"]),
+                        "est_total_s": repr(p["estimate"]["total_s"]), "padding_fraction": repr(p["padding_fraction"])})
+    return buf.getvalue()
 
 
 def loopnest_text(doc: dict, index: int = 0) -> str:
@@ -368,22 +392,29 @@ def _parser() -> argparse.ArgumentParser:
             p.add_argument("--range", action="append")
             p.add_argument("--psi", type=float)
             p.add_argument("--coeffs")
-            p.add_argument("--workers", type=int, default=1)
+            p.add_argument("--workers", type=int)
         p.add_argument("--out")
 
     common(sub.add_parser("tune", help="compile stage -> candidate cache"))
     p = sub.add_parser("plan", help="combine + SIA Top-K -> plan report")
     common(p)
     p.add_argument("--cache")
-    p.add_argument("--topk", type=int, default=10)
-    p.add_argument("--emit", choices=["plan", "loopnest"], default="plan")
-    p.add_argument("--index", type=int, default=0)
+    p.add_argument("--topk", type=int)
+    p.add_argument("--emit", choices=["plan", "loopnest", "csv"])
+    p.add_argument("--index", type=int)
+    p.add_argument("--timings", help="write combine + rank wall-clock to this file (keeps the plan report "
+                                     "byte-identical across runs)")
     p = sub.add_parser("emit-loopnest", help="plan report -> tiled loop nest text")
     common(p, workload=False)
     p.add_argument("--plan")
-    p.add_argument("--index", type=int, default=0)
+    p.add_argument("--index", type=int)
     common(sub.add_parser("sweep", help="per-shape CSV over a range"))
     return ap
+
+
+# Flag defaults, applied AFTER the FTB_CLI_* environment overrides: a flag
+# given on the command line wins, then the environment, then these.
+DEFAULTS = {"workers": 1, "topk": 10, "emit": "plan", "index": 0}
 
 
 def _env_defaults(args) -> None:
@@ -393,6 +424,10 @@ def _env_defaults(args) -> None:
             if env is not None:
                 setattr(args, k, env.split(";") if k in ("shape", "range") else
                         (int(env) if k in ("topk", "index", "workers") else (float(env) if k == "psi" else env)))
+            elif k in DEFAULTS:
+                setattr(args, k, DEFAULTS[k])
+    if getattr(args, "emit", None) not in (None, "plan", "loopnest", "csv"):
+        raise ValueError(f"--emit / FTB_CLI_EMIT must be plan, loopnest or csv, not {args.emit!r}")
 
 
 def main(argv: list[str] | None = None) -> int:

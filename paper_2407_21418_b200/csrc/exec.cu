@@ -195,6 +195,44 @@ void split(int64_t lo, int64_t hi, int64_t maxlen, std::vector<Piece>& out, int6
 
 }  // namespace
 
+// Per-device resources of the table allocator: tables live in the device's
+// stream-ordered memory pool (cudaMallocAsync / cudaFreeAsync, pool kept
+// resident), uploaded on a private non-blocking stream and released on
+// another one after every launch that used them — no cudaMalloc, no
+// synchronous cudaMemcpy and no cudaFree (each of which would synchronise the
+// whole device) on the create / destroy path.
+struct DeviceRes {
+  cudaStream_t upload = nullptr;
+  cudaStream_t reclaim = nullptr;
+};
+static DeviceRes& device_res(int dev) {
+  static std::mutex mu;
+  static DeviceRes res[64];
+  std::lock_guard<std::mutex> g(mu);
+  DeviceRes& r = res[dev & 63];
+  if (!r.upload) {
+    FTB_CUDA(cudaStreamCreateWithFlags(&r.upload, cudaStreamNonBlocking));
+    FTB_CUDA(cudaStreamCreateWithFlags(&r.reclaim, cudaStreamNonBlocking));
+    cudaMemPool_t pool;
+    if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+      uint64_t keep = UINT64_MAX;  // freed tables stay in the pool for the next create
+      cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
+    }
+  }
+  return r;
+}
+
+// Host image of one table allocation: sections appended at 128-B offsets.
+struct Blob {
+  std::vector<uint8_t> bytes;
+  size_t add(const void* src, size_t n) {
+    const size_t off = (bytes.size() + 127) & ~static_cast<size_t>(127);
+    bytes.resize(off + n);
+    if (src && n) std::memcpy(bytes.data() + off, src, n);
+    return off;
+  }
+};
+
 struct ExecImpl {
   std::vector<DevProblem> problems;
   std::vector<DevMaps> maps;          // tcgen05: TMA descriptors per problem
@@ -208,21 +246,42 @@ struct ExecImpl {
   TcWork* d_tcwork = nullptr;
   TcPair* d_tcpairs = nullptr;
   float* d_split_ws = nullptr;        // split-K fp32 partials
-  int32_t* d_split_cnt = nullptr;     // split-K arrival counters (self-resetting)
+  int32_t* d_split_cnt = nullptr;     // split-K chunk counters (self-resetting)
   unsigned long long* d_trace = nullptr;
+  void* d_blob = nullptr;             // one pool allocation: every section above but the workspace
+  int device = -1;
+  // streams this table was launched on, each with the event recorded after
+  // its last launch: destroy frees only after all of them (stream order)
+  std::vector<std::pair<cudaStream_t, cudaEvent_t>> launched;
+  cudaStream_t last_stream = nullptr;
+  std::mutex mu;     // launches may come from several host threads
   TcConfig cfg{};    // single-CTA kernel (K1)
   TcConfig cfg2{};   // CTA-pair kernel (K1b)
   int64_t n_singles = 0, n_pairs = 0, ctas1 = 0, ctas2 = 0;
   ftb_exec_info info{};
   ~ExecImpl() {
-    if (d_problems) cudaFree(d_problems);
-    if (d_work) cudaFree(d_work);
-    if (d_maps) cudaFree(d_maps);
-    if (d_tcwork) cudaFree(d_tcwork);
-    if (d_tcpairs) cudaFree(d_tcpairs);
-    if (d_split_ws) cudaFree(d_split_ws);
-    if (d_split_cnt) cudaFree(d_split_cnt);
-    if (d_trace) cudaFree(d_trace);
+    if (device < 0) {
+      if (d_trace) cudaFree(d_trace);
+      return;
+    }
+    int cur = -1;
+    cudaGetDevice(&cur);
+    if (cur != device) cudaSetDevice(device);
+    cudaStream_t rs = nullptr;
+    try {
+      rs = device_res(device).reclaim;
+    } catch (...) {
+    }
+    for (auto& se : launched) {
+      if (rs) cudaStreamWaitEvent(rs, se.second, 0);
+      cudaEventDestroy(se.second);  // the wait above captured its state
+    }
+    if (rs) {
+      if (d_blob) cudaFreeAsync(d_blob, rs);
+      if (d_split_ws) cudaFreeAsync(d_split_ws, rs);
+    }
+    if (d_trace) cudaFree(d_trace);  // debug builds only (ftb_exec_set_trace)
+    if (cur >= 0 && cur != device) cudaSetDevice(cur);
   }
 };
 
@@ -452,17 +511,31 @@ static void build(ExecImpl& ex, const ftb_gemm_desc* probs, const ftb_program* p
 // Device upload: problems (FFMA) or TMA descriptors + self-contained items
 // (tcgen05), and the per-launch pipeline shape from the widest item.
 static void upload(ExecImpl& I) {
-  FTB_CUDA(cudaMalloc(&I.d_problems, sizeof(DevProblem) * I.problems.size()));
-  FTB_CUDA(cudaMemcpy(I.d_problems, I.problems.data(), sizeof(DevProblem) * I.problems.size(),
-                      cudaMemcpyHostToDevice));
-  if (I.work.empty()) return;
-  if (I.info.kernel == 1) {
-    FTB_CUDA(cudaMalloc(&I.d_work, sizeof(DevWork) * I.work.size()));
-    FTB_CUDA(cudaMemcpy(I.d_work, I.work.data(), sizeof(DevWork) * I.work.size(), cudaMemcpyHostToDevice));
+  FTB_CUDA(cudaGetDevice(&I.device));
+  const cudaStream_t us = device_res(I.device).upload;
+  // one pool allocation for the whole table, filled by one async copy on the
+  // private upload stream; create returns once that copy has landed (a wait
+  // on this stream only — kernels running on other streams are not waited for)
+  auto commit = [&](Blob& b) {
+    FTB_CUDA(cudaMallocAsync(&I.d_blob, std::max<size_t>(b.bytes.size(), 128), us));
+    FTB_CUDA(cudaMemcpyAsync(I.d_blob, b.bytes.data(), b.bytes.size(), cudaMemcpyHostToDevice, us));
+    FTB_CUDA(cudaStreamSynchronize(us));
+  };
+  auto at = [&](size_t off) { return static_cast<uint8_t*>(I.d_blob) + off; };
+  if (I.work.empty() || I.info.kernel == 1) {
+    Blob b;
+    const size_t op = b.add(I.problems.data(), sizeof(DevProblem) * I.problems.size());
+    const size_t ow = b.add(I.work.data(), sizeof(DevWork) * I.work.size());
+    commit(b);
+    I.d_problems = reinterpret_cast<DevProblem*>(at(op));
+    I.d_work = reinterpret_cast<DevWork*>(at(ow));
     return;
   }
-  FTB_CUDA(cudaMalloc(&I.d_maps, sizeof(DevMaps) * I.maps.size()));
-  FTB_CUDA(cudaMemcpy(I.d_maps, I.maps.data(), sizeof(DevMaps) * I.maps.size(), cudaMemcpyHostToDevice));
+  // work records reference their problem's descriptors by device address;
+  // until the allocation exists they carry the problem index (fixed up below)
+  auto maps_of = [](int32_t problem) {
+    return reinterpret_cast<const DevMaps*>(static_cast<uintptr_t>(problem));
+  };
   auto flags_of = [](const DevProblem& P) {
     return (P.swap ? kFlagSwap : 0u) | (P.lane_mn ? kFlagLaneMN : 0u) | (P.col_mn ? kFlagColMN : 0u) |
            (P.out_f32 ? kFlagOutF32 : 0u) | ((P.bias || P.act) ? kFlagEpiOp : 0u);
@@ -507,7 +580,7 @@ static void upload(ExecImpl& I) {
       const DevProblem& P = I.problems[w.problem];
       TcPair t;
       std::memset(&t, 0, sizeof(t));
-      t.maps = I.d_maps + w.problem;
+      t.maps = maps_of(w.problem);
       t.C = c_of(P, w.batch);
       t.ldc = P.ldc;
       t.lane0[0] = a.lane0;
@@ -526,6 +599,7 @@ static void upload(ExecImpl& I) {
     }
   }
   std::vector<TcWork> tw;
+  int32_t split_tiles = 0;  // tiles whose split-K partials meet in the global workspace
   int max_n = 16;
   for (size_t i = 0; i < I.work.size(); ++i) {
     if (paired[i]) continue;
@@ -547,7 +621,7 @@ static void upload(ExecImpl& I) {
       for (size_t q = i; q < j; ++q) ok = ok && tma_ok(I.work[q]);
       TcWork t;
       std::memset(&t, 0, sizeof(t));
-      t.maps = I.d_maps + w.problem;
+      t.maps = maps_of(w.problem);
       t.C = c_of(P, w.batch);
       t.ldc = P.ldc;
       t.lane0 = w.lane0;
@@ -568,7 +642,7 @@ static void upload(ExecImpl& I) {
     }
     TcWork t;
     std::memset(&t, 0, sizeof(t));
-    t.maps = I.d_maps + w.problem;
+    t.maps = maps_of(w.problem);
     t.C = c_of(P, w.batch);
     t.ldc = P.ldc;
     t.lane0 = w.lane0;
@@ -584,8 +658,8 @@ static void upload(ExecImpl& I) {
   }
   // Split-K: a table too small to occupy the SMs (e.g. one skinny Dense, or a
   // mid-size shape timed alone) splits each plain item's K blocks over up to
-  // kMaxSplit items; partials meet in an fp32 workspace and the last warp to
-  // arrive per lane quadrant reduces and stores (kernel_tc.cu). Tables that
+  // kMaxSplit items; partials meet in an fp32 workspace and the last split to
+  // publish each 32-column chunk reduces and stores it (kernel_tc.cu). Tables that
   // already fill the GPU (the grouped C1 step) are left alone.
   // Column split: a table with fewer than half as many items as SMs runs one
   // wave whose length is one item's K loop; a 256-column item's K block costs
@@ -688,15 +762,15 @@ static void upload(ExecImpl& I) {
           split.push_back(u);
         }
       }
-      // the split epilogue's all-splits rendezvous needs every item resident
-      // at once: one item per CTA, at most one CTA per SM
+      // one wave (<= one item per SM) keeps a tile's splits concurrent so the
+      // per-chunk reductions spread over them; correctness does not depend on
+      // it (the last split to publish a chunk reduces it, nobody waits)
       if (tiles > 0 && s_cl) {
         I.cfg.cluster_split = s_cl;  // partials stay on chip: no workspace
         tw.swap(split);
       } else if (tiles > 0 && static_cast<int64_t>(split.size()) <= sms_here) {
-        FTB_CUDA(cudaMalloc(&I.d_split_ws, sizeof(float) * static_cast<size_t>(tiles) * kSplitTileFloats));
-        FTB_CUDA(cudaMalloc(&I.d_split_cnt, sizeof(int32_t) * 8 * tiles));
-        FTB_CUDA(cudaMemset(I.d_split_cnt, 0, sizeof(int32_t) * 8 * tiles));
+        FTB_CUDA(cudaMallocAsync(&I.d_split_ws, sizeof(float) * static_cast<size_t>(tiles) * kSplitTileFloats, us));
+        split_tiles = tiles;
         tw.swap(split);
       }
     }
@@ -760,13 +834,28 @@ static void upload(ExecImpl& I) {
   }
   I.n_singles = static_cast<int64_t>(tw.size());
   I.n_pairs = static_cast<int64_t>(pairs.size());
-  if (!tw.empty()) {
-    FTB_CUDA(cudaMalloc(&I.d_tcwork, sizeof(TcWork) * tw.size()));
-    FTB_CUDA(cudaMemcpy(I.d_tcwork, tw.data(), sizeof(TcWork) * tw.size(), cudaMemcpyHostToDevice));
-  }
-  if (!pairs.empty()) {
-    FTB_CUDA(cudaMalloc(&I.d_tcpairs, sizeof(TcPair) * pairs.size()));
-    FTB_CUDA(cudaMemcpy(I.d_tcpairs, pairs.data(), sizeof(TcPair) * pairs.size(), cudaMemcpyHostToDevice));
+  {
+    Blob b;
+    const size_t op = b.add(nullptr, sizeof(DevProblem) * I.problems.size());
+    const size_t om = b.add(nullptr, sizeof(DevMaps) * I.maps.size());
+    const size_t ot = b.add(nullptr, sizeof(TcWork) * tw.size());
+    const size_t oq = b.add(nullptr, sizeof(TcPair) * pairs.size());
+    const size_t oc = b.add(nullptr, sizeof(int32_t) * kSplitCntPerTile * static_cast<size_t>(split_tiles));
+    FTB_CUDA(cudaMallocAsync(&I.d_blob, std::max<size_t>(b.bytes.size(), 128), us));
+    I.d_problems = reinterpret_cast<DevProblem*>(at(op));
+    I.d_maps = reinterpret_cast<DevMaps*>(at(om));
+    I.d_tcwork = tw.empty() ? nullptr : reinterpret_cast<TcWork*>(at(ot));
+    I.d_tcpairs = pairs.empty() ? nullptr : reinterpret_cast<TcPair*>(at(oq));
+    I.d_split_cnt = split_tiles ? reinterpret_cast<int32_t*>(at(oc)) : nullptr;
+    for (TcWork& t : tw) t.maps = I.d_maps + reinterpret_cast<uintptr_t>(t.maps);
+    for (TcPair& t : pairs) t.maps = I.d_maps + reinterpret_cast<uintptr_t>(t.maps);
+    std::memcpy(b.bytes.data() + op, I.problems.data(), sizeof(DevProblem) * I.problems.size());
+    std::memcpy(b.bytes.data() + om, I.maps.data(), sizeof(DevMaps) * I.maps.size());
+    if (!tw.empty()) std::memcpy(b.bytes.data() + ot, tw.data(), sizeof(TcWork) * tw.size());
+    if (!pairs.empty()) std::memcpy(b.bytes.data() + oq, pairs.data(), sizeof(TcPair) * pairs.size());
+    // split-K counters start at zero (the Blob is zero-filled) and re-arm themselves
+    FTB_CUDA(cudaMemcpyAsync(I.d_blob, b.bytes.data(), b.bytes.size(), cudaMemcpyHostToDevice, us));
+    FTB_CUDA(cudaStreamSynchronize(us));
   }
   int sms = device_sms();
   if (sms <= 0) sms = 148;
@@ -830,6 +919,22 @@ ftb_status ftb_exec_launch(ftb_exec* ex, void* stream) {
     if (!ex) throw ftb::input_error("null exec");
     auto& I = ex->impl;
     cudaStream_t s = static_cast<cudaStream_t>(stream);
+    std::lock_guard<std::mutex> g(I.mu);
+    int cur = -1;
+    FTB_CUDA(cudaGetDevice(&cur));
+    if (I.device >= 0 && cur != I.device)
+      throw ftb::input_error("the table lives on device " + std::to_string(I.device) + ", the current device is " +
+                             std::to_string(cur), "device");
+    cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
+    FTB_CUDA(cudaStreamIsCapturing(s, &cap));
+    const bool capturing = cap != cudaStreamCaptureStatusNone;
+    // Launches of one table are stream ordered (they share the split-K
+    // workspace): a launch on a new stream first waits for the previous one.
+    // Captured launches are not tracked — a graph holding this table must not
+    // outlive it (as with any buffer the graph references).
+    if (!capturing && I.last_stream && I.last_stream != s)
+      for (auto& se : I.launched)
+        if (se.first == I.last_stream) FTB_CUDA(cudaStreamWaitEvent(s, se.second, 0));
     cudaError_t e = I.info.kernel == 1
                         ? ftb::launch_ffma(I.d_problems, I.d_work, static_cast<int32_t>(I.info.n_work),
                                            static_cast<int32_t>(I.info.n_ctas), s)
@@ -839,6 +944,17 @@ ftb_status ftb_exec_launch(ftb_exec* ex, void* stream) {
     if (e == cudaSuccess && I.info.kernel == 0 && I.n_singles)
       e = ftb::launch_tc(I.d_tcwork, static_cast<int32_t>(I.n_singles), static_cast<int32_t>(I.ctas1), I.cfg, s);
     if (e != cudaSuccess) throw ftb::cuda_error(std::string("kernel launch: ") + cudaGetErrorString(e));
+    if (!capturing) {  // destroy frees the table only after this launch (exec.cu ~ExecImpl)
+      cudaEvent_t ev = nullptr;
+      for (auto& se : I.launched)
+        if (se.first == s) ev = se.second;
+      if (!ev) {
+        FTB_CUDA(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+        I.launched.emplace_back(s, ev);
+      }
+      FTB_CUDA(cudaEventRecord(ev, s));
+      I.last_stream = s;
+    }
   });
 }
 

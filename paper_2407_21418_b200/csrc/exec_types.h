@@ -79,8 +79,9 @@ struct alignas(16) DevWork {
 //   hardware) instead of predicated st.global.
 //   kFlagSplitK: the item computes K blocks [kb0, kb0 + num_kb) of a tile split
 //   over nsplit items (pack = kb0 | nsplit << 16 | split << 24, c_bs = tile);
-//   partials meet in the fp32 workspace and the last warp per lane quadrant
-//   to arrive sums them and stores C (exec.cu, kernel_tc.cu).
+//   partials meet in the fp32 workspace chunk by chunk (32 columns of one lane
+//   quadrant); the last split to publish a chunk sums it and stores C, so no
+//   split ever waits for another (no co-residency assumption; kernel_tc.cu).
 enum : uint32_t {
   kFlagSwap = 1u, kFlagLaneMN = 2u, kFlagColMN = 4u, kFlagOutF32 = 8u, kFlagTmaStore = 16u, kFlagSplitK = 32u,
   kFlagEpiOp = 64u  // fused bias / activation: maps->epi
@@ -112,6 +113,8 @@ __host__ __device__ inline int split_idx(uint32_t p) { return static_cast<int>(p
 constexpr int kMaxSplit = 8;
 constexpr int kSplitRowFloats = 256;                          // columns per tile in the workspace
 constexpr int kSplitTileFloats = kMaxSplit * 128 * kSplitRowFloats;
+constexpr int kSplitChunks = kSplitRowFloats / 32;            // 32-column chunks per tile row
+constexpr int kSplitCntPerTile = 4 * kSplitChunks;            // one arrival counter per (lane quadrant, chunk)
 
 // CTA-pair work item (64 B): two 128-lane slabs (one per CTA of a cluster
 // pair) that share the column operand; N = n_mma columns, each CTA stages
@@ -136,7 +139,7 @@ struct TcConfig {
   int32_t acc_cols;        // columns per slot (512 / n_acc)
   unsigned long long* trace;  // optional: per-CTA phase timestamps (debug)
   float* split_ws;            // split-K partials [tile][split][128][256] fp32
-  int32_t* split_cnt;         // split-K counters [tile][arrive, depart][4 lane quadrants]
+  int32_t* split_cnt;         // split-K arrival counters [tile][4 lane quadrants][8 chunks]
   int32_t cluster_split;      // > 1: split-K partials reduced on chip across a cluster of this many CTAs
   int32_t epi8;               // 1: eight epilogue warps (two groups on alternate items), 320 threads
 };

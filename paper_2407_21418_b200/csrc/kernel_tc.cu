@@ -77,10 +77,10 @@ __device__ __forceinline__ TcWork bcast_work(uint32_t mine) {
 }
 
 // Split-K epilogue for one warp (lane quadrant): publish the fp32 partial of
-// this split to the workspace, count the arrival; the last of the tile's
-// splits for this quadrant sums all partials (fixed split order, so the sum is
-// deterministic) and stores C through the predicated path, then re-arms the
-// counter for the next launch.
+// this split to the workspace and count its arrival per 32-column chunk; the
+// split completing a chunk sums all partials of it (fixed split order, so the
+// sum is deterministic) and stores C through the predicated path, then
+// re-arms the chunk's counter for the next launch.
 template <bool kCluster, class Release>
 __device__ __forceinline__ void split_epilogue(const TcConfig& cfg, const TcWork& it, uint8_t* region, uint32_t taddr,
                                                int lane_base, bool swap, bool f32, Release release, float* csmem) {
@@ -109,36 +109,40 @@ __device__ __forceinline__ void split_epilogue(const TcConfig& cfg, const TcWork
   auto part = [&](int split, int c0) {
     return ws + ((static_cast<size_t>(split) * 4 + quad) * (kSplitRowFloats / 32) + (c0 >> 5)) * 1024 + lane;
   };
-  for (int c0 = 0; c0 < it.col_len; c0 += 32) {
+  const bool active = lane_base < it.lane_len;  // the same for every split of the tile
+  // pass 1: publish this split's fp32 partial, then hand TMEM back
+  for (int c0 = 0; active && c0 < it.col_len; c0 += 32) {
     uint32_t raw[32];
     tmem_ld_32x32b_x32(taddr + c0, raw);
     tmem_ld_wait();
     float* dst = part(me, c0);
 #pragma unroll
-    for (int e = 0; e < 32; ++e) dst[e * 32] = __uint_as_float(raw[e]);
+    for (int e = 0; e < 32; ++e) __stcg(dst + e * 32, __uint_as_float(raw[e]));
   }
   release();  // TMEM no longer needed
+  if (!active) return;
   __threadfence();
   __syncwarp();
-  // All splits of a tile are resident at once (split-K is only planned for
-  // tables of <= one item per SM, exec.cu), so every split warp of this
-  // quadrant waits for the others' partials and then reduces its share of
-  // the 32-column chunks: the reduction runs on nsplit warps in parallel
-  // instead of serially on the last to arrive.
-  int32_t* arrive = cfg.split_cnt + tile * 8 + quad;
-  int32_t* depart = arrive + 4;
-  if (lane == 0) {
-    atomicAdd(arrive, 1);
-    while (ld_acquire_gpu(arrive) < nsplit) __nanosleep(32);
-  }
-  __syncwarp();
-  __threadfence();
+  // pass 2: count arrivals per 32-column chunk; the split whose arrival
+  // completes a chunk reduces it (fixed split order: the sum is bit-identical
+  // whoever reduces) and stores C. No split waits for another, so split-K
+  // needs no co-residency (a concurrent kernel holding SMs only delays the
+  // last arrival). Chunks are visited in an order rotated by the split index
+  // so that, when the splits finish together, the reductions spread over
+  // them instead of landing on one warp.
+  int32_t* cnt = cfg.split_cnt + static_cast<size_t>(tile) * kSplitCntPerTile + quad * kSplitChunks;
   float* tb = reinterpret_cast<float*>(region);
   if (lane == 0) bulk_wait_read<0>();  // the transpose tile aliases this warp's store boxes
   __syncwarp();
-  const int c_first = me * 32;
-  const int c_step = nsplit * 32;
-  for (int c0 = (lane_base < it.lane_len) ? c_first : it.col_len; c0 < it.col_len; c0 += c_step) {
+  const int nch = (it.col_len + 31) >> 5;
+  for (int j = 0; j < nch; ++j) {
+    const int ch = (me + j) % nch;
+    int prev = 0;
+    if (lane == 0) prev = atomicAdd(cnt + ch, 1);
+    prev = __shfl_sync(0xffffffffu, prev, 0);
+    if (prev != nsplit - 1) continue;
+    __threadfence();  // every other split's partial of this chunk is visible
+    const int c0 = ch * 32;
     float v[32];
 #pragma unroll
     for (int e = 0; e < 32; ++e) v[e] = 0.f;
@@ -162,6 +166,7 @@ __device__ __forceinline__ void split_epilogue(const TcConfig& cfg, const TcWork
 #pragma unroll
       for (int e = 0; e < 32; ++e) v[e] += __ldcg(src + e * 32);
     }
+    if (lane == 0) cnt[ch] = 0;  // every split has counted: re-arm for the next launch
     if (it.flags & kFlagEpiOp) {
       uint32_t rb[32];
 #pragma unroll
@@ -176,13 +181,6 @@ __device__ __forceinline__ void split_epilogue(const TcConfig& cfg, const TcWork
       store_block32(tb, v, true, it.C, it.ldc, it.lane0 + lane_base, it.col0 + c0, nlane, ncol, f32);
     else
       store_block32(tb, v, false, it.C, it.ldc, it.col0 + c0, it.lane0 + lane_base, ncol, nlane, f32);
-  }
-  // the last warp out re-arms both counters for the next launch (stream
-  // order, or griddepcontrol.wait under PDL, separates launches)
-  __syncwarp();
-  if (lane == 0 && atomicAdd(depart, 1) == nsplit - 1) {
-    *arrive = 0;
-    *depart = 0;
   }
 }
 
@@ -576,13 +574,8 @@ int tc_smem_bytes(const TcConfig& cfg) {
 template <int S, bool kCluster, bool kEpi8>
 static cudaError_t launch_tc_sk(const TcWork* work, int32_t n_work, int32_t n_ctas, TcConfig cfg,
                                 cudaStream_t stream) {
-  static bool configured = false;
-  if (!configured) {
-    cudaError_t e = cudaFuncSetAttribute(ftb_tc_kernel<S, kCluster, kEpi8>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         232448);
-    if (e != cudaSuccess) return e;
-    configured = true;
-  }
+  cudaError_t e = configure_smem_once<ftb_tc_kernel<S, kCluster, kEpi8>>(232448);
+  if (e != cudaSuccess) return e;
   return launch_pdl_cluster(ftb_tc_kernel<S, kCluster, kEpi8>, n_ctas, kEpi8 ? kTcThreadsEpi8 : kTcThreads,
                             tc_smem_bytes(cfg), kCluster ? cfg.cluster_split : 1, stream, work, n_work, cfg);
 }

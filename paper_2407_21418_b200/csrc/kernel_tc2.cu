@@ -287,12 +287,8 @@ int tc_smem_bytes(const TcConfig& cfg);
 template <int S>
 static cudaError_t launch_tc2_s(const TcPair* work, int32_t n_work, int32_t n_ctas, TcConfig cfg,
                                 cudaStream_t stream) {
-  static bool configured = false;
-  if (!configured) {
-    cudaError_t e = cudaFuncSetAttribute(ftb_tc2_kernel<S>, cudaFuncAttributeMaxDynamicSharedMemorySize, 232448);
-    if (e != cudaSuccess) return e;
-    configured = true;
-  }
+  cudaError_t e = configure_smem_once<ftb_tc2_kernel<S>>(232448);
+  if (e != cudaSuccess) return e;
   return launch_pdl(ftb_tc2_kernel<S>, n_ctas, kTcThreads, tc_smem_bytes(cfg), stream, work, n_work, cfg);
 }
 

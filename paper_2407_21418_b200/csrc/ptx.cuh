@@ -7,10 +7,28 @@
 // mirrored in CUTLASS's cute/arch/mma_sm100_desc.hpp (SmemDescriptor,
 // InstrDescriptor), which is the only on-disk reference in this image.
 #pragma once
+#include <atomic>
 #include <cstdint>
 #include <cuda.h>
+#include <cuda_runtime.h>
 
 namespace ftb {
+
+// cudaFuncSetAttribute(MaxDynamicSharedMemorySize) is per device: remember it
+// per (kernel, device) so a process that launches on several GPUs configures
+// each one (a process-wide flag would skip every device but the first).
+template <auto Kernel>
+inline cudaError_t configure_smem_once(int bytes) {
+  static std::atomic<uint64_t> done{0};
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return e;
+  const uint64_t bit = 1ull << (dev & 63);
+  if (done.load(std::memory_order_acquire) & bit) return cudaSuccess;
+  e = cudaFuncSetAttribute(Kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+  if (e == cudaSuccess) done.fetch_or(bit, std::memory_order_acq_rel);
+  return e;
+}
 
 __device__ __forceinline__ uint32_t smem_addr(const void* p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));

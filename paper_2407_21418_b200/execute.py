@@ -91,25 +91,44 @@ def gemm_desc(A, B, Cout, b_layout: str = "kn", orientation: int = -1, bias=None
     (Dense only).
     """
     d = GemmDesc()
+    if b_layout not in ("kn", "nk"):
+        raise ValueError(f"b_layout must be 'kn' or 'nk', not {b_layout!r}")
+    # The TMA descriptors and the work table are built from these extents, not
+    # from the allocations: every operand must agree with them, or the kernel
+    # would read past B or write past Cout (torch.matmul raises here too).
     if A.dim() == 2:
         d.op, d.batch = OP_DENSE, 1
         M, K = A.shape
-        N = B.shape[1] if b_layout == "kn" else B.shape[0]
+        if B.dim() != 2 or Cout.dim() != 2:
+            raise ValueError("Dense needs 2-D A, B and C")
+        Kb, N = (B.shape[0], B.shape[1]) if b_layout == "kn" else (B.shape[1], B.shape[0])
+        if tuple(Cout.shape) != (M, N):
+            raise ValueError(f"C has shape {tuple(Cout.shape)}, expected {(M, N)}")
         d.a_batch_stride = d.b_batch_stride = d.c_batch_stride = 0
         rows = lambda t: t.stride(0)  # noqa: E731
     elif A.dim() == 3:
         d.op = OP_BMM
         d.batch, M, K = A.shape
-        N = B.shape[2] if b_layout == "kn" else B.shape[1]
+        if B.dim() != 3 or Cout.dim() != 3:
+            raise ValueError("BatchMatmul needs 3-D A, B and C")
+        Kb, N = (B.shape[1], B.shape[2]) if b_layout == "kn" else (B.shape[2], B.shape[1])
+        if B.shape[0] != d.batch:
+            raise ValueError(f"B has batch {B.shape[0]}, A has {d.batch}")
+        if tuple(Cout.shape) != (d.batch, M, N):
+            raise ValueError(f"C has shape {tuple(Cout.shape)}, expected {(d.batch, M, N)}")
         d.a_batch_stride, d.b_batch_stride, d.c_batch_stride = A.stride(0), B.stride(0), Cout.stride(0)
         rows = lambda t: t.stride(1)  # noqa: E731
     else:
         raise ValueError("A must be 2-D (dense) or 3-D (batch matmul)")
+    if Kb != K:
+        raise ValueError(f"inner dimensions differ: A has K={K}, B has K={Kb} (b_layout={b_layout!r})")
     for name, t in (("A", A), ("B", B), ("C", Cout)):
         if t.stride(-1) != 1:
             raise ValueError(f"{name} must be contiguous in its last dimension")
         if not t.is_cuda:
             raise ValueError(f"{name} must be a CUDA tensor (the executor has no CPU path)")
+        if t.device != A.device:
+            raise ValueError(f"{name} is on {t.device}, A on {A.device}: one problem lives on one device")
     d.M, d.N, d.K = int(M), int(N), int(K)
     d.A, d.B, d.C = A.data_ptr(), B.data_ptr(), Cout.data_ptr()
     d.lda, d.ldb, d.ldc = rows(A), rows(B), rows(Cout)
@@ -122,12 +141,21 @@ def gemm_desc(A, B, Cout, b_layout: str = "kn", orientation: int = -1, bias=None
     if bias is not None:
         if bias.dim() != 1 or bias.shape[0] != d.N or not bias.is_cuda or bias.stride(0) != 1:
             raise ValueError("bias must be a contiguous CUDA vector of length N")
+        if bias.device != A.device:
+            raise ValueError(f"bias is on {bias.device}, A on {A.device}")
         d.bias = bias.data_ptr()
         d.bias_dtype = _dt(bias)
     if activation not in (None, "none", "gelu"):
         raise ValueError(f"unsupported activation {activation!r} (None or 'gelu')")
     d.activation = _lib.ACT_GELU if activation == "gelu" else _lib.ACT_NONE
+    d.device_index = A.device.index if A.device.index is not None else _current_device()
     return d
+
+
+def _current_device() -> int:
+    import torch
+
+    return torch.cuda.current_device()
 
 
 # --------------------------------------------------------------------- executable
@@ -159,15 +187,24 @@ class Executable:
     """
 
     def __init__(self, descs: Sequence[GemmDesc], programs: Sequence[Program], keepalive=()):
+        import torch
+
         L = _lib.lib()
         n = len(descs)
         if n != len(programs) or n == 0:
             raise ValueError("need one program per problem")
+        devs = {getattr(d, "device_index", None) for d in descs} - {None}
+        if len(devs) > 1:
+            raise ValueError(f"one table runs on one device; problems span devices {sorted(devs)}")
+        # the table, its TMA descriptors and the launch belong to the tensors'
+        # device, whatever the caller's current device is
+        self.device = torch.device("cuda", devs.pop() if devs else torch.cuda.current_device())
         self._descs = (GemmDesc * n)(*descs)
         self._progs = (Program * n)(*programs)
         self._keep = list(keepalive)
         h = C.c_void_p()
-        _lib.check(L.ftb_exec_create(self._descs, self._progs, n, C.byref(h)))
+        with torch.cuda.device(self.device):
+            _lib.check(L.ftb_exec_create(self._descs, self._progs, n, C.byref(h)))
         self._h = h
         info = _lib.ExecInfo()
         _lib.check(L.ftb_exec_get_info(self._h, C.byref(info)))
@@ -179,8 +216,11 @@ class Executable:
     def launch(self, stream=None) -> None:
         import torch
 
-        s = stream if stream is not None else torch.cuda.current_stream()
-        _lib.check(_lib.lib().ftb_exec_launch(self._h, C.c_void_p(s.cuda_stream)))
+        s = stream if stream is not None else torch.cuda.current_stream(self.device)
+        if s.device != self.device:
+            raise ValueError(f"stream is on {s.device}, the table on {self.device}")
+        with torch.cuda.device(self.device):
+            _lib.check(_lib.lib().ftb_exec_launch(self._h, C.c_void_p(s.cuda_stream)))
 
     def config(self) -> dict:
         """Pipeline shape chosen for this table (tcgen05 kernel)."""

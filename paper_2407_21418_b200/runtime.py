@@ -169,18 +169,23 @@ class Planner:
     # ---------------------------------------------------------------- ops
 
     def _launch(self, rec, A, B, out, b_layout, bias=None, activation=None, stream=None):
-        """Launch one planned problem through a small cache of lowered tables
-        (keyed by the buffers: TMA descriptors embed their addresses). Cached
-        tables keep their buffers alive, so a key is never reused by another
-        tensor at the same address while cached."""
-        key = tuple((t.data_ptr(), tuple(t.shape), tuple(t.stride()), t.dtype) if t is not None else None
-                    for t in (A, B, out, bias)) + (b_layout, activation, id(rec))
+        """Launch one planned problem through a small cache of lowered tables.
+
+        TMA descriptors embed buffer addresses, so the key holds each tensor's
+        (address, shape, strides, dtype, device). The cache does NOT keep the
+        tensors alive: a cached table is only ever launched again for tensors
+        matching its key exactly — the same bytes it was built for — so a
+        freed-and-reused address is harmless, and evicting a table never
+        synchronises the device (exec.cu frees it in stream order after its
+        last launch)."""
+        key = tuple((t.data_ptr(), tuple(t.shape), tuple(t.stride()), t.dtype, t.device)
+                    if t is not None else None for t in (A, B, out, bias)) + (b_layout, activation, id(rec))
         with self._lock:
             ex = self._exe_cache.pop(key, None)
         if ex is None:
             ex = Executable([gemm_desc(A, B, out, b_layout, bias=bias, activation=activation)], [rec.program],
-                            (A, B, out, bias, rec))
-        ex.launch(stream)
+                            (rec,))
+        ex.launch(stream if stream is not None else _current_stream(A.device))
         with self._lock:
             self._exe_cache[key] = ex
             while len(self._exe_cache) > self.exe_cache_size:
@@ -238,6 +243,12 @@ class Planner:
                                                             row["fallback_stage"], row["counts"])
             n += 1
         return n
+
+
+def _current_stream(device):
+    import torch
+
+    return torch.cuda.current_stream(device)
 
 
 _FFMA = None

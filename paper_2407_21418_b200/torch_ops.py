@@ -129,10 +129,9 @@ def execute_table(As: List[torch.Tensor], Bs: List[torch.Tensor], b_layouts: str
         outs.append(torch.empty(shape, dtype=_out_dtype(A), device=A.device))
         descs.append(gemm_desc(A, B, outs[-1], lay))
     recs = pl.plan(insts)
-    ex = Executable(descs, [r.program for r in recs], (*As, *Bs, *outs))
-    ex.launch(torch.cuda.current_stream())
-    torch.cuda.current_stream().synchronize()  # the table is freed below
-    ex.close()
+    ex = Executable(descs, [r.program for r in recs])
+    ex.launch(torch.cuda.current_stream(As[0].device))
+    ex.close()  # freed in stream order after the launch: no host or device sync
     return outs
 
 

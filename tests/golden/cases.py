@@ -51,4 +51,13 @@ CASES = [
     # V100-like descriptor (the paper's target) incl. a capped (truncated) enumeration
     _c("v100_m53", "v100_like", dense_doc(768, 768, 4, 128), {"i": 53}),
     _c("v100_m64_cap", "v100_like", dense_doc(768, 768, 4, 128), {"i": 64}, cap=40000),
+    # big pools (5.9M-201M plans): Top-10 from the streaming
+    # oracle of reference primitives only (the reference cannot materialise them)
+    _c("c2_scores_t257", "b200_bf16", bmm_doc(1024, (1, 512), (1, 512), 64), {"i": 257, "j": 257}, topk_stream=True, big=True),
+    _c("c2_scores_t512", "b200_bf16", bmm_doc(1024, (1, 512), (1, 512), 64), {"i": 512, "j": 512}, topk_stream=True, big=True),
+    _c("c2_context_t512", "b200_bf16", bmm_doc(1024, (1, 512), 64, (1, 512)), {"i": 512, "k": 512}, topk_stream=True, big=True),
+    _c("c3_m4096", "b200_bf16", dense_doc(4096, 4096, 2), {"i": 4096}, topk_stream=True, big=True),
+    _c("c3_m8191", "b200_bf16", dense_doc(4096, 4096, 2), {"i": 8191}, topk_stream=True, big=True),
+    _c("c1_ffn1_m1696", "b200_bf16", dense_doc(3072, 768, 2), {"i": 1696}, topk_stream=True, big=True),
+    _c("c1_out_m1696", "b200_bf16", dense_doc(768, 768, 2), {"i": 1696}, topk_stream=True, big=True),
 ]

@@ -39,12 +39,13 @@ from cases import CASES  # noqa: E402
 POOL_MATERIALISE_MAX = 400_000
 
 
-def streaming_topk(kernels, inst, k=10, coeffs=None):
-    """Top-k of rank_programs(build_programs(kernels, inst)) from reference primitives."""
+def streaming_topk(kernels, inst, k=10, coeffs=None, tau=None):
+    """Top-k of rank_programs(build_programs(kernels, inst)) from reference
+    primitives; ``tau`` overrides select_main_axis (B200 fallback rung 1)."""
     coeffs = coeffs or SiaCoeffs()
     spec = inst.spec
     space, axes = spec.space_axes, tuple(spec.space_axes) + tuple(spec.reduce_axes)
-    tau = select_main_axis(inst)
+    tau = select_main_axis(inst) if tau is None else tau
     H = inst.extent(tau)
     uniq = {}
     for kk in kernels:
@@ -215,9 +216,27 @@ def kats():
 
 
 def main():
-    only = set(sys.argv[1:])
+    """make_golden.py [ids...]            run cases into planner_cases.json
+    make_golden.py --part DIR ids...     cases into DIR/<id>.json (for parallel runs)
+    make_golden.py --merge DIR           merge DIR/*.json into planner_cases.json"""
     out_p = HERE / "planner_cases.json"
     existing = json.loads(out_p.read_text()) if out_p.exists() else {}
+    if sys.argv[1:2] == ["--part"]:
+        part = Path(sys.argv[2])
+        part.mkdir(parents=True, exist_ok=True)
+        for case in CASES:
+            if case["id"] in sys.argv[3:]:
+                t0 = time.time()
+                res = run_case(case)
+                (part / f"{case['id']}.json").write_text(json.dumps(res, indent=1, sort_keys=True) + "\n")
+                print(f"{case['id']}: {time.time() - t0:.1f}s pool={res['pool_size']}", flush=True)
+        return
+    if sys.argv[1:2] == ["--merge"]:
+        for p in sorted(Path(sys.argv[2]).glob("*.json")):
+            existing[p.stem] = json.loads(p.read_text())
+        out_p.write_text(json.dumps(existing, indent=1, sort_keys=True) + "\n")
+        return
+    only = set(sys.argv[1:])
     for case in CASES:
         if only and case["id"] not in only:
             continue

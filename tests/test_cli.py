@@ -171,3 +171,35 @@ def test_env_overrides(monkeypatch, capsys):
     monkeypatch.setenv("FTB_CLI_RANGE", "i=1..3")
     rc, out, _ = run(capsys, "sweep")
     assert rc == 0 and len(out.strip().splitlines()) == 4
+
+
+def test_plan_report_is_byte_identical_and_timings_go_elsewhere(tmp_path, capsys):
+    """SPEC invariant "All commands are deterministic": the plan report holds
+    no wall-clock; --timings writes the combine + rank times to its own file."""
+    a, b, t = tmp_path / "a.json", tmp_path / "b.json", tmp_path / "t.json"
+    for p in (a, b):
+        rc, _, err = run(capsys, "plan", "--workload", "dense:768:768", "--range", "i=50..53", "--topk", "3",
+                         "--out", str(p), "--timings", str(t))
+        assert rc == 0, err
+    assert a.read_bytes() == b.read_bytes()
+    assert "timing" not in a.read_text()
+    tim = json.loads(t.read_text())
+    assert tim["kind"] == "plan-timings" and len(tim["shapes"]) == 4
+    assert all(s["combine_rank_s"] >= 0 for s in tim["shapes"])
+
+
+def test_env_overrides_flags_that_have_defaults(tmp_path, capsys, monkeypatch):
+    """FTB_CLI_* applies to --topk / --emit too (defaults resolve after the
+    environment); a flag on the command line still wins."""
+    out = tmp_path / "p.json"
+    monkeypatch.setenv("FTB_CLI_TOPK", "2")
+    assert run(capsys, "plan", "--workload", "dense:768:768", "--shape", "i=53", "--out", str(out))[0] == 0
+    assert len(json.loads(out.read_text())["shapes"][0]["plans"]) == 2
+    assert run(capsys, "plan", "--workload", "dense:768:768", "--shape", "i=53", "--topk", "4",
+               "--out", str(out))[0] == 0
+    assert len(json.loads(out.read_text())["shapes"][0]["plans"]) == 4
+    monkeypatch.setenv("FTB_CLI_EMIT", "csv")
+    assert run(capsys, "plan", "--workload", "dense:768:768", "--shape", "i=53", "--out", str(out))[0] == 0
+    rows = list(csv.DictReader(io.StringIO(out.read_text())))
+    assert [int(r["rank"]) for r in rows] == [0, 1]
+    assert all(r["binding"] == "i=53" for r in rows)
