@@ -661,6 +661,60 @@ static void upload(ExecImpl& I) {
   // kMaxSplit items; partials meet in an fp32 workspace and the last split to
   // publish each 32-column chunk reduces and stores it (kernel_tc.cu). Tables that
   // already fill the GPU (the grouped C1 step) are left alone.
+  // Wide on-chip split-K: a table that fills at most half the SMs with
+  // long-K items (e.g. one C1 Dense timed alone: 15-36 128 x 256 tiles of
+  // 12-48 K blocks) runs one wave whose length is one item's whole K loop.
+  // Splitting every item's K range 4 (or 2) ways into a cluster of that many
+  // CTAs keeps the full 256-column MMA (the cheapest per FLOP) and cuts the
+  // wave to a quarter (half) of the K loop; the splits' fp32 partials (up to
+  // 128 KiB, parked in each CTA's idle operand ring) are reduced through
+  // distributed shared memory (kernel_tc.cu cluster_reduce). Needs every
+  // item splittable (>= FTB_SPLIT_CL_MINKB K blocks per split, default 3)
+  // and the table within the co-resident clusters (measured: 33 clusters of
+  // 4, 74 of 2, scripts/micro/cluster_occ.cu). OPT-IN (FTB_SPLIT_WIDE_CLUSTER=1):
+  // measured on B200 it LOSES — C1 out M=608 6.3 -> 11.8 us, FFN2 M=1024
+  // 13.5 -> 15.7 us (profiles/r2g_wide_cluster_split_chain_time.txt): parking a 128 x 256 fp32
+  // partial in smem takes ~1.5 us and the DSMEM pull reduction ~7 us
+  // (scripts/chain_trace.py), far more than the K blocks it parallelises.
+  bool wide_split = false;
+  {
+    int sms_here = device_sms();
+    if (sms_here <= 0) sms_here = 148;
+    const char* env_w = std::getenv("FTB_SPLIT_WIDE_CLUSTER");
+    const char* env_sk = std::getenv("FTB_SPLITK");
+    const char* env_cl = std::getenv("FTB_SPLIT_CLUSTER");
+    const bool on = (env_w && env_w[0] == '1') && !(env_sk && env_sk[0] == '0') && !(env_cl && env_cl[0] == '0') &&
+                    !pairing;
+    const char* env_mk = std::getenv("FTB_SPLIT_CL_MINKB");
+    const int cl_min = env_mk ? std::max(1, std::atoi(env_mk)) : 3;
+    const int64_t n = static_cast<int64_t>(tw.size());
+    if (on && n > 0 && n * 2 <= sms_here) {
+      for (int cand : {4, 2}) {
+        const int64_t cap = std::min<int64_t>(cand == 4 ? 132 : 148, sms_here);
+        if (n * cand > cap) continue;
+        bool ok = true;
+        for (const TcWork& t : tw) ok = ok && !t.pack && t.num_kb >= cand * cl_min;
+        if (!ok) continue;
+        std::vector<TcWork> split;
+        split.reserve(n * cand);
+        for (const TcWork& t : tw)
+          for (int q = 0; q < cand; ++q) {
+            TcWork u = t;
+            const int kb0 = static_cast<int>(static_cast<int64_t>(t.num_kb) * q / cand);
+            const int kb1 = static_cast<int>(static_cast<int64_t>(t.num_kb) * (q + 1) / cand);
+            u.num_kb = kb1 - kb0;
+            u.flags |= kFlagSplitK;
+            u.pack = static_cast<uint32_t>(kb0) | (static_cast<uint32_t>(cand) << 16) | (static_cast<uint32_t>(q) << 24);
+            u.c_bs = 0;
+            split.push_back(u);
+          }
+        I.cfg.cluster_split = cand;
+        tw.swap(split);
+        wide_split = true;
+        break;
+      }
+    }
+  }
   // Column split: a table with fewer than half as many items as SMs runs one
   // wave whose length is one item's K loop; a 256-column item's K block costs
   // ~550 clk (smem-port bound: 48 KiB TMA write + 48 KiB MMA read), a
@@ -674,7 +728,7 @@ static void upload(ExecImpl& I) {
     const bool cs_on = !(env_cs && env_cs[0] == '0') && !pairing;
     int64_t wide = 0;
     for (const TcWork& t : tw) wide += (!t.pack && t.n_mma > 128 && t.col_len > 128) ? 1 : 0;
-    if (cs_on && wide > 0 && static_cast<int64_t>(tw.size()) + wide <= sms_here) {
+    if (!wide_split && cs_on && wide > 0 && static_cast<int64_t>(tw.size()) + wide <= sms_here) {
       std::vector<TcWork> cs;
       cs.reserve(tw.size() + wide);
       for (const TcWork& t : tw) {
@@ -707,7 +761,7 @@ static void upload(ExecImpl& I) {
     const int split_min_kb = env_mk ? std::max(1, std::atoi(env_mk)) : 8;
     const char* env_w = std::getenv("FTB_SPLIT_WIDE");
     const bool split_wide = env_w && env_w[0] == '1';
-    if (split_on && n_items > 0 && n_items * 2 <= sms_here) {
+    if (!wide_split && split_on && n_items > 0 && n_items * 2 <= sms_here) {
       const int target = static_cast<int>(std::min<int64_t>(kMaxSplit, sms_here / n_items));
       // On-chip mode: when every item can be split the same way (s = 4 or 2,
       // >= split_min_kb K blocks per split) and the whole table fits the
@@ -879,6 +933,10 @@ static void upload(ExecImpl& I) {
     c.trace = nullptr;
   };
   shape_cfg(I.cfg, max_n, max_n);
+  {
+    const char* env_pf = std::getenv("FTB_L2_PREFETCH");
+    I.cfg.l2_prefetch = (env_pf && env_pf[0] == '0') ? 0 : 1;
+  }
   I.cfg.split_ws = I.d_split_ws;
   I.cfg.split_cnt = I.d_split_cnt;
   int max_np = 32;

@@ -142,6 +142,7 @@ struct TcConfig {
   int32_t* split_cnt;         // split-K arrival counters [tile][4 lane quadrants][8 chunks]
   int32_t cluster_split;      // > 1: split-K partials reduced on chip across a cluster of this many CTAs
   int32_t epi8;               // 1: eight epilogue warps (two groups on alternate items), 320 threads
+  int32_t l2_prefetch;        // 1: L2-prefetch the first item's operands before griddepcontrol.wait
 };
 constexpr int kTraceItems = 16;   // items traced per CTA
 constexpr int kTraceEvents = 6;   // see kernel_tc.cu

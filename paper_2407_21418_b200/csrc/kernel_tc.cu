@@ -89,15 +89,32 @@ __device__ __forceinline__ void split_epilogue(const TcConfig& cfg, const TcWork
   if (kCluster) {
     // On-chip mode: the splits of a tile are the CTAs of one cluster, one item
     // each. This split's fp32 partial goes to this CTA's (now idle) operand
-    // ring, [quad][chunk][32 cols][32 lanes]; cluster_reduce sums the cluster's
-    // partials after the kernel's closing cluster barrier.
-    for (int c0 = 0; c0 < it.col_len; c0 += 32) {
-      uint32_t raw[32];
-      tmem_ld_32x32b_x32(taddr + c0, raw);
+    // ring: per (chunk, quad) a 4 KiB block laid out [column group g of 4][lane][4],
+    // so each v4 store here and each v4 DSMEM load of cluster_reduce moves
+    // 512 contiguous bytes per warp (coalesced; a lane-strided layout made
+    // every remote load 32 separate 16-B packets and the reduction 2x
+    // slower). cluster_reduce sums the cluster's partials after the kernel's
+    // closing cluster barrier.
+    for (int c0 = 0; c0 < it.col_len; c0 += 64) {
+      const bool two = c0 + 32 < it.col_len;
+      uint32_t ra[32], rb[32];
+      tmem_ld_32x32b_x32(taddr + c0, ra);
+      if (two) tmem_ld_32x32b_x32(taddr + c0 + 32, rb);
       tmem_ld_wait();
-      float* dst = csmem + ((quad * 4 + (c0 >> 5)) * 32) * 32 + lane;  // <= 4 chunks (n_mma <= 128): 64 KiB
+      float* blk = csmem + (static_cast<size_t>((c0 >> 5) * 4 + quad) << 10) + lane * 4;
 #pragma unroll
-      for (int e = 0; e < 32; ++e) dst[e * 32] = __uint_as_float(raw[e]);
+      for (int g = 0; g < 8; ++g)
+        *reinterpret_cast<float4*>(blk + g * 128) =
+            make_float4(__uint_as_float(ra[4 * g]), __uint_as_float(ra[4 * g + 1]), __uint_as_float(ra[4 * g + 2]),
+                        __uint_as_float(ra[4 * g + 3]));
+      if (two) {
+        blk += 4 * 1024;  // next chunk, same quad
+#pragma unroll
+        for (int g = 0; g < 8; ++g)
+          *reinterpret_cast<float4*>(blk + g * 128) =
+              make_float4(__uint_as_float(rb[4 * g]), __uint_as_float(rb[4 * g + 1]), __uint_as_float(rb[4 * g + 2]),
+                          __uint_as_float(rb[4 * g + 3]));
+      }
     }
     release();
     return;
@@ -187,42 +204,83 @@ __device__ __forceinline__ void split_epilogue(const TcConfig& cfg, const TcWork
 // On-chip split-K reduction (cfg.cluster_split > 1): CTA `rank` of the
 // cluster sums chunks rank, rank + s, ... of its lane quadrant over the s
 // partials held in the cluster's shared memories (distributed shared memory,
-// fixed split order: deterministic), then applies the fused epilogue op and
-// stores C through the coalesced predicated path.
+// 16-B loads, two peers in flight; fixed split order: deterministic and
+// bit-identical to the workspace path at the same split count), applies the
+// fused epilogue op and stores C — through TMA store boxes when the item
+// allows it, else the coalesced predicated path.
 __device__ __forceinline__ void cluster_reduce(const TcConfig& cfg, const TcWork& it, uint8_t* region, float* csmem,
                                                int quad) {
   const int lane = threadIdx.x & 31;
   const int lane_base = quad * 32;
   if (lane_base >= it.lane_len) return;
   const bool swap = it.flags & kFlagSwap, f32 = it.flags & kFlagOutF32;
+  const bool tma = (it.flags & kFlagTmaStore) && !f32;
   const int s = cfg.cluster_split;
   const int rank = static_cast<int>(cluster_ctarank());
   float* tb = reinterpret_cast<float*>(region);
   if (lane == 0) bulk_wait_read<0>();  // the transpose tile aliases this warp's store boxes
   __syncwarp();
   const int nch = (it.col_len + 31) >> 5;
+  uint32_t nbox = 0;
   for (int ch = rank; ch < nch; ch += s) {
     float v[32];
 #pragma unroll
     for (int e = 0; e < 32; ++e) v[e] = 0.f;
-    const uint32_t mine = smem_addr(csmem + ((quad * 4 + ch) * 32) * 32 + lane);
-    for (int p = 0; p < s; ++p) {
+    const uint32_t mine = smem_addr(csmem + (static_cast<size_t>(ch * 4 + quad) << 10) + lane * 4);
+    int p = 0;
+    for (; p + 2 <= s; p += 2) {
       const uint32_t pa = mapa_shared(mine, static_cast<uint32_t>(p));
-      float a[32];
+      const uint32_t pb = mapa_shared(mine, static_cast<uint32_t>(p + 1));
+      float4 a[8], b[8];
 #pragma unroll
-      for (int e = 0; e < 32; ++e) a[e] = ld_dsmem_f32(pa + e * 128);
+      for (int g = 0; g < 8; ++g) {
+        a[g] = ld_dsmem_v4(pa + g * 512);
+        b[g] = ld_dsmem_v4(pb + g * 512);
+      }
 #pragma unroll
-      for (int e = 0; e < 32; ++e) v[e] += a[e];
+      for (int g = 0; g < 8; ++g) {
+        v[4 * g] = (v[4 * g] + a[g].x) + b[g].x;
+        v[4 * g + 1] = (v[4 * g + 1] + a[g].y) + b[g].y;
+        v[4 * g + 2] = (v[4 * g + 2] + a[g].z) + b[g].z;
+        v[4 * g + 3] = (v[4 * g + 3] + a[g].w) + b[g].w;
+      }
+    }
+    if (p < s) {
+      const uint32_t pa = mapa_shared(mine, static_cast<uint32_t>(p));
+      float4 a[8];
+#pragma unroll
+      for (int g = 0; g < 8; ++g) a[g] = ld_dsmem_v4(pa + g * 512);
+#pragma unroll
+      for (int g = 0; g < 8; ++g) {
+        v[4 * g] += a[g].x;
+        v[4 * g + 1] += a[g].y;
+        v[4 * g + 2] += a[g].z;
+        v[4 * g + 3] += a[g].w;
+      }
     }
     const int c0 = ch * 32;
-    if (it.flags & kFlagEpiOp) {
-      uint32_t rb[32];
+    uint32_t rb[32];
 #pragma unroll
-      for (int e = 0; e < 32; ++e) rb[e] = __float_as_uint(v[e]);
-      apply_epi(rb, it.maps->epi, !swap, swap ? it.lane0 + lane_base : it.col0 + c0);
-#pragma unroll
-      for (int e = 0; e < 32; ++e) v[e] = __uint_as_float(rb[e]);
+    for (int e = 0; e < 32; ++e) rb[e] = __float_as_uint(v[e]);
+    if (it.flags & kFlagEpiOp) apply_epi(rb, it.maps->epi, !swap, swap ? it.lane0 + lane_base : it.col0 + c0);
+    if (tma) {
+      uint8_t* box = region + (nbox & 3) * 2048;
+      if (lane == 0 && nbox >= 4) bulk_wait_read<3>();  // this box's previous store has read it
+      __syncwarp();
+      stage_box_bf16(box, rb, !swap);
+      fence_async_smem();
+      __syncwarp();
+      if (lane == 0) {
+        const int l0 = it.lane0 + lane_base, k0 = it.col0 + c0;
+        if (!swap) tma_store_3d(&it.maps->out, smem_addr(box), k0, l0, it.batch);
+        else tma_store_3d(&it.maps->out, smem_addr(box), l0, k0, it.batch);
+        bulk_commit();
+      }
+      ++nbox;
+      continue;
     }
+#pragma unroll
+    for (int e = 0; e < 32; ++e) v[e] = __uint_as_float(rb[e]);
     const int ncol = min(32, it.col_len - c0);
     const int nlane = min(32, it.lane_len - lane_base);
     if (!swap)
@@ -230,6 +288,8 @@ __device__ __forceinline__ void cluster_reduce(const TcConfig& cfg, const TcWork
     else
       store_block32(tb, v, false, it.C, it.ldc, it.col0 + c0, it.lane0 + lane_base, ncol, nlane, f32);
   }
+  if (lane == 0) bulk_wait_read<0>();
+  __syncwarp();
 }
 
 // kCluster: the on-chip split-K variant (cluster launch, one item per CTA);
@@ -313,6 +373,44 @@ __global__ void __launch_bounds__(kEpi8 ? 384 : kTcThreads, 1)
     if (lane == 0 && static_cast<int>(blockIdx.x) < n_work) {
       tma_prefetch_desc(&cur.maps->lane);
       tma_prefetch_desc(&cur.maps->col[0]);
+      // Programmatic dependent launch: this grid runs ahead of its
+      // predecessor's tail. Pull the first item's first K block of operand
+      // boxes from HBM into L2 now, so the first loads issued after
+      // griddep_wait hit L2 instead of paying the DRAM latency on the
+      // launch's critical path (1-item chain: 4.08 -> 3.58 us, profiles/r2j_l2_prefetch_ab.txt).
+      if (cfg.l2_prefetch && cur.num_kb <= 2) {  // short items only: measured, long-K Dense
+                                                 // items lost ~4 % with it (the prefetch's TMA
+                                                 // issue sits on their critical path)
+        const bool pk = !(cur.flags & kFlagSplitK) && pack_depth(cur.pack);
+        const int kb0 = (cur.flags & kFlagSplitK) ? split_kb0(cur.pack) : 0;
+        const int nkb = 1;  // the first K block only: later ones stream behind it (a whole
+                            // ring's worth cost 96-CTA tables ~1.3 us, profiles/profiles/r2j_l2_prefetch_ab.txt)
+        const uint32_t cmask = col_box_mask(cur.n_mma);
+        for (int kb = 0; kb < nkb; ++kb) {
+          const int k0 = (kb + kb0) * kBlockK;
+          if (pk || !(cur.flags & kFlagLaneMN)) {
+            tma_prefetch_l2_3d(&cur.maps->lane, k0, cur.lane0, cur.batch);
+          } else {
+            tma_prefetch_l2_3d(&cur.maps->lane, cur.lane0, k0, cur.batch);
+            tma_prefetch_l2_3d(&cur.maps->lane, cur.lane0 + 64, k0, cur.batch);
+          }
+          if (!(cur.flags & kFlagColMN)) {
+            if (pk) {
+              tma_prefetch_l2_3d(&cur.maps->col[0], k0, cur.col0, cur.batch);
+            } else {
+              int r = 0;
+              for (int q = 0; q < kColMaps; ++q)
+                if (cmask & (1u << q)) {
+                  tma_prefetch_l2_3d(&cur.maps->col[q], k0, cur.col0 + r, cur.batch);
+                  r += 256 >> q;
+                }
+            }
+          } else {
+            const int ncol = pk ? 64 : cur.n_mma;
+            for (int c = 0; c < ncol; c += 64) tma_prefetch_l2_3d(&cur.maps->col[0], cur.col0 + c, k0, cur.batch);
+          }
+        }
+      }
     }
     griddep_wait();
     for (int w = blockIdx.x; w < n_work; w += G, ++local) {
@@ -357,6 +455,9 @@ __global__ void __launch_bounds__(kEpi8 ? 384 : kTcThreads, 1)
         c_wait += cs - cw;
 #endif
         if (lane == 0) {
+#ifdef FTB_TRACE_PRE
+          trace_kb(cfg, g, 0);  // debug: stamp BEFORE the K block's TMA issue
+#endif
           // one lane issues: measured faster here than the converged elect form
           // (619 vs 504 clk per K block, scripts/prod_profile.py)
           mbar_arrive_expect_tx(&full[s], bytes);
@@ -385,7 +486,9 @@ __global__ void __launch_bounds__(kEpi8 ? 384 : kTcThreads, 1)
             }
           }
           if (kb == 0) trace_ev(cfg, local, 1);
+#ifndef FTB_TRACE_PRE
           trace_kb(cfg, g, 0);
+#endif
         }
         __syncwarp();
 #ifdef FTB_PROD_PROFILE
@@ -550,11 +653,23 @@ __global__ void __launch_bounds__(kEpi8 ? 384 : kTcThreads, 1)
   tc_fence_before();
   __syncthreads();
   if (kCluster) {  // one item per CTA: reduce the cluster's split-K partials on chip
+#ifdef FTB_TRACE
+    if (threadIdx.x == 64) trace_kb(cfg, 60, 0);  // debug: before the first cluster barrier
+#endif
     cluster_sync();              // every split's partial written (release / acquire at cluster scope)
+#ifdef FTB_TRACE
+    if (threadIdx.x == 64) trace_kb(cfg, 60, 1);
+#endif
     if (warp >= 2 && static_cast<int>(blockIdx.x) < n_work)
       cluster_reduce(cfg, load_work(work, blockIdx.x), reinterpret_cast<uint8_t*>(epi_buf) + (warp & 3) * kEpiWarpBytes,
                      reinterpret_cast<float*>(smem), warp & 3);
+#ifdef FTB_TRACE
+    if (threadIdx.x == 64) trace_kb(cfg, 61, 0);  // debug: warp 2 done reducing
+#endif
     cluster_sync();              // peers have read this CTA's partial before it exits
+#ifdef FTB_TRACE
+    if (threadIdx.x == 64) trace_kb(cfg, 61, 1);
+#endif
   }
 #ifdef FTB_TRACE
   if (threadIdx.x == 0 && cfg.trace)  // CTA end stamp (all epilogue stores issued and complete)
