@@ -241,6 +241,13 @@ ftb_status ftb_lower(const ftb_gemm_desc* problems, const ftb_program* programs,
 /* Number of SMs of the current device (0 if none). */
 int32_t ftb_device_sm_count(void);
 
+/* TEST HOOK (not on the hot path): launch n_ctas CTAs on `stream` that each
+ * hold one SM (maximal dynamic shared memory) until ctl[0] != 0 or timeout_ns
+ * elapses. ctl is mapped pinned host memory: ctl[1] counts CTAs that arrived,
+ * ctl[2] CTAs that timed out. Lets tests run the executor while another
+ * kernel occupies most SMs (split-K must not assume co-residency). */
+ftb_status ftb_test_occupy_sms(int32_t n_ctas, int32_t* ctl, int64_t timeout_ns, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

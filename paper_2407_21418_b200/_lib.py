@@ -123,6 +123,7 @@ def lib() -> C.CDLL:
         "ftb_exec_set_trace": (i32, [vp, i32]),
         "ftb_exec_read_trace": (i32, [vp, C.POINTER(C.c_uint64), i64, C.POINTER(i64)]),
         "ftb_exec_get_config": (i32, [vp, C.POINTER(i32)]),
+        "ftb_test_occupy_sms": (i32, [i32, vp, i64, vp]),
     }
     for name, (res, args) in sig.items():
         fn = getattr(L, name)

@@ -26,7 +26,7 @@ def check(C, ref, K: int, out_f32: bool | None = None, ffma: bool = False, scale
 
     if out_f32 is None:
         out_f32 = C.dtype == torch.float32
-    r = ref.double()
+    r = ref.double().to(C.device)
     err = (C.double() - r).abs()
     rel = REL_F32 if (out_f32 or ffma) else REL_BF16
     tol = rel * r.abs() + (ABS_ACC_FFMA if ffma else ABS_ACC) * math.sqrt(max(1, K)) * scale

@@ -1,0 +1,64 @@
+"""Split-K without a co-residency assumption (VERDICT r1 weak #6 / ADVICE):
+a split-K table runs on one stream while another kernel holds all but a few
+SMs and only lets go AFTER the split-K launch has finished. The round-1
+rendezvous (every split spins until all splits of its tile arrive) would
+deadlock here — the resident splits wait for splits that cannot be scheduled
+— until the occupier's timeout; the per-chunk last-arriver reduction runs
+the splits in waves on the free SMs and completes. Both the on-chip cluster
+path and the global-workspace path are exercised; results must be correct
+and identical to the same table launched on an idle GPU."""
+
+import ctypes
+import time
+
+import pytest
+import torch
+
+from _numerics import assert_close
+from paper_2407_21418_b200 import _lib
+from paper_2407_21418_b200.execute import Executable, gemm_desc, program_struct
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.mark.parametrize("cluster", ["0", "1"])
+def test_split_k_completes_while_other_kernel_holds_sms(cuda, monkeypatch, cluster):
+    monkeypatch.setenv("FTB_SPLIT_CLUSTER", cluster)
+    M, N, K = 64, 1024, 4096
+    g = torch.Generator(device="cpu").manual_seed(9)
+    A = (torch.rand(M, K, generator=g) * 2 - 1).bfloat16().to(cuda)
+    B = (torch.rand(N, K, generator=g) * 2 - 1).bfloat16().to(cuda)
+    ref = A.double() @ B.double().t()
+    C = torch.full((M, N), float("nan"), dtype=torch.bfloat16, device=cuda)
+    ex = Executable([gemm_desc(A, B, C, "nk")], [program_struct(2, 1, [((1, 1), (64, 256, 64), 4)])])
+    ex.launch()
+    torch.cuda.synchronize()
+    alone = C.clone()
+    assert_close(alone, ref, K, "idle GPU")
+    n_split_ctas = ex.info.n_ctas
+    sms = torch.cuda.get_device_properties(cuda).multi_processor_count
+    free = 4
+    assert n_split_ctas > free, "the table must need more SMs than are left free"
+    ctl = torch.zeros(4, dtype=torch.int32).pin_memory()
+    occ_stream, run_stream = torch.cuda.Stream(cuda), torch.cuda.Stream(cuda)
+    L = _lib.lib()
+    _lib.check(L.ftb_test_occupy_sms(sms - free, ctypes.c_void_p(ctl.data_ptr()), int(20e9),
+                                     ctypes.c_void_p(occ_stream.cuda_stream)))
+    t0 = time.time()
+    while ctl[1].item() < sms - free and time.time() - t0 < 10:
+        time.sleep(1e-3)
+    assert ctl[1].item() == sms - free, "occupier did not become resident"
+    C.fill_(float("nan"))
+    torch.cuda.current_stream(cuda).synchronize()
+    ex.launch(run_stream)
+    done = torch.cuda.Event()
+    done.record(run_stream)
+    t0 = time.time()
+    while not done.query() and time.time() - t0 < 15:
+        time.sleep(1e-3)
+    finished = done.query()
+    ctl[0] = 1  # release the occupier either way (it also gives up after 20 s)
+    torch.cuda.synchronize()
+    assert finished, "split-K launch did not finish while the other kernel held the SMs"
+    assert ctl[2].item() == 0, "occupier timed out"
+    assert torch.equal(C, alone)
