@@ -504,8 +504,57 @@ def run_ours(args, rank, world, local):
                                           f"over the same {cb['shapes']}-shape set, {cb['passes']} passes, "
                                           f"{cb['seconds']:.1f} s of compute"}
     line["per_shape"] = ps["rows"] if args.per_shape_rows else None
+    if args.c4_shapes > 0:
+        line["c4_sweep"] = c4_sweep(args, rank, world, dev, P)
     if rank == 0:
         print(json.dumps(line), flush=True)
+
+
+def c4_sweep(args, rank, world, dev, P):
+    """North_star config 5: a fixed sample of the C4 10k-shape dynamic
+    Dense/BMM sweep (identical on every rank, seed 0) LPT-partitioned by
+    roofline time across the N ranks (strong scaling: total work fixed),
+    each rank planning and executing ONLY its bucket (grouped launches of
+    <= 12 GB chunks, shard.make_gpu_executor), with no collective on the data
+    path; per-shape records (plan, tuning s, output checksum) are gathered to
+    rank 0 over NCCL at the end and every checksum is verified there against
+    its size-independent expectation sum(C) = 1^T A B 1. Kernel time is the
+    sum of the rank's timed chunk launches; the sweep time is its max over
+    ranks."""
+    import torch
+
+    from paper_2407_21418_b200.runtime import Planner
+    from paper_2407_21418_b200.shard import checksum_ok, make_gpu_executor, run_sharded
+    from paper_2407_21418_b200.workloads import c4_shapes
+
+    shapes = c4_shapes(args.c4_shapes, seed=0)
+    planner = Planner()
+    ex = make_gpu_executor(planner, dev)
+    barrier(world)
+    t0 = time.perf_counter()
+    buckets, merged = run_sharded(shapes, rank, world, planner, P, execute=ex)
+    wall = time.perf_counter() - t0
+    torch.cuda.synchronize(dev)
+    kernel_ms = max_over_ranks(ex.stats["kernel_ms"], world)
+    wall = max_over_ranks(wall, world)
+    out = None
+    if rank == 0:
+        import json as _json
+
+        flops = sum(s.flops for s in shapes)
+        t_roof = sum(s.t_roof(P) for s in shapes)
+        cs = [_json.loads(r.checksum) for r in merged]
+        bad = [r.index for r, c in zip(merged, cs) if not checksum_ok(c)]
+        out = {"n_shapes": len(shapes), "n_gpus": world, "scaling": "strong",
+               "tflops": flops / (kernel_ms * 1e-3) / 1e12, "kernel_ms": kernel_ms,
+               "roofline_frac": (t_roof / world) / (kernel_ms * 1e-3),
+               "roofline_def": "(sum of per-shape t_roof / N) / max-over-ranks kernel time",
+               "bucket_sizes": [len(b) for b in buckets],
+               "tuning_s_sum": sum(r.tuning_s for r in merged),
+               "checksums_verified": len(cs) - len(bad), "checksum_failures": bad[:20],
+               "gathered_records": len(merged), "wall_s_max_rank": wall,
+               "chunks_rank0": ex.stats["chunks"], "launches_rank0": ex.stats["launches"]}
+    return out
 
 
 def main():
@@ -519,6 +568,8 @@ def main():
     ap.add_argument("--per-shape-rows", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--ops", choices=["all", "dense", "bmm"], default="all")
+    ap.add_argument("--c4-shapes", type=int, default=2000,
+                    help="C4 sweep sample size (0 skips the c4_sweep key; 10000 = the full north_star set)")
     args = ap.parse_args()
     args.warmup = max(3, args.warmup)
     if args.impl == "reference":

@@ -5,6 +5,7 @@ end-to-end runs. Used by bench.py, smoke() and the GPU tests."""
 from __future__ import annotations
 
 import time
+import zlib
 from dataclasses import dataclass, field
 
 from .execute import Executable, gemm_desc
@@ -46,13 +47,18 @@ class Bound:
 
 class ShapeSet:
     def __init__(self, shapes: list[Shape], planner: Planner | None = None, device="cuda", seed: int = 0,
-                 pinned: bool = False):
+                 pinned: bool = False, seeds: list[int] | None = None, records=None):
+        """``seeds``: one seed per shape — its activations are drawn from it and
+        every weight from a hash of its (name, N, K, layout) key, so a shape's
+        data does not depend on which other shapes share the set (the sharded
+        C4 sweep checks per-shape checksums across partitions). ``records``:
+        plans already made (skips planning)."""
         import torch
 
         self.shapes = shapes
         self.planner = planner or Planner()
         t0 = time.perf_counter()
-        self.records = self.planner.plan([s.instance() for s in shapes])
+        self.records = records if records is not None else self.planner.plan([s.instance() for s in shapes])
         self.tuning_s = time.perf_counter() - t0
         self.device = torch.device(device)
         g = torch.Generator(device=self.device)
@@ -81,15 +87,33 @@ class ShapeSet:
         self._in_sizes, self._out_sizes, self._dt = in_sizes, out_sizes, dt
         in_views, self.in_arena = _arena([sh for xs in in_sizes for sh in xs], dt, self.device)
         out_views, self.out_arena = _arena(out_sizes, dt, self.device)
-        self.in_arena.copy_(rnd(self.in_arena.numel()))
+        if seeds is None:
+            self.in_arena.copy_(rnd(self.in_arena.numel()))
+        else:
+            off = 0
+            for sd, sizes in zip(seeds, in_sizes):
+                for sh_ in sizes:
+                    v = in_views[off]
+                    off += 1
+                    gs = torch.Generator(device=self.device)
+                    gs.manual_seed(int(sd))
+                    v.copy_((torch.rand(v.numel(), generator=gs, device=self.device) * 2 - 1).to(dt).view_as(v))
+
+        def weight(key, *shape):
+            if seeds is None:
+                return rnd(*shape)
+            gw = torch.Generator(device=self.device)
+            gw.manual_seed(zlib.crc32(repr(key).encode()))
+            return (torch.rand(*shape, generator=gw, device=self.device, dtype=torch.float32) * 2 - 1).to(dt)
+
         k = 0
         for s, oc in zip(shapes, out_views):
             if s.kind == "dense":
                 A = in_views[k]
                 k += 1
-                key = (s.name, s.N, s.K)
+                key = (s.name, s.N, s.K, s.b_layout)
                 if key not in weights:
-                    weights[key] = rnd(s.N, s.K) if s.b_layout == "nk" else rnd(s.K, s.N)
+                    weights[key] = weight(key, s.N, s.K) if s.b_layout == "nk" else weight(key, s.K, s.N)
                 B = weights[key]
                 self.bound.append(Bound(s, A, B, oc, A, oc, [A]))
             elif s.name == "scores":  # Q [b,T,64] @ K^T, K given as [b,T,64] ("nk")
@@ -207,6 +231,18 @@ class ShapeSet:
 
     def padding_ratio(self) -> float:
         return self.exe.info.padding_ratio
+
+    def checksums(self) -> list[dict]:
+        """Per shape, on the device in float64: the sum of C and its
+        size-independent expectation sum_k colsum(A)[k] * rowsum(B)[k]
+        (= 1^T A B 1), plus sum |C| as the scale."""
+        out = []
+        for x in self.bound:
+            Bkn = x.B.double().transpose(-1, -2) if x.shape.b_layout == "nk" else x.B.double()
+            C = x.C.double()
+            expect = (x.A.double().sum(-2) * Bkn.sum(-1)).sum()
+            out.append({"sum": float(C.sum()), "expect": float(expect), "abs": float(C.abs().sum())})
+        return out
 
     def reference_outputs(self, idx: int):
         """fp64 torch result of shape idx (for numerics checks on device)."""

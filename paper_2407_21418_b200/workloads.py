@@ -49,6 +49,14 @@ class Shape:
         """Algorithmic HBM bytes: inputs once + output once."""
         return self.in_bytes * self.batch * (self.M * self.K + self.K * self.N) + self.out_bytes * self.batch * self.M * self.N
 
+    @property
+    def bytes_padded(self) -> int:
+        """Device bytes a ShapeSet allocates for this shape (rows padded to 8)."""
+        r8 = lambda n: (n + 7) // 8 * 8  # noqa: E731
+        ob = self.out_bytes * self.batch * self.M * (r8(self.N) if self.name == "scores" else self.N)
+        ib = self.in_bytes * self.batch * (self.M * r8(self.K) + self.K * self.N)
+        return ib + ob
+
     def t_roof(self, peak_flops: float) -> float:
         return max(self.flops / peak_flops, self.bytes / HBM_ROOF_BPS)
 
