@@ -14,8 +14,11 @@
 
 #include <algorithm>
 #include <array>
+#include <chrono>
+#include <cstdio>
 #include <cstdlib>
 #include <map>
+#include <memory>
 #include <cstring>
 #include <mutex>
 #include <string>
@@ -222,6 +225,60 @@ static DeviceRes& device_res(int dev) {
   return r;
 }
 
+// Pinned staging for table uploads (per device): the table is copied into a
+// reusable pinned chunk and sent with one cudaMemcpyAsync on the private
+// upload stream; create returns without waiting for it (the first launch
+// waits on the table's `ready` event on the device side). A chunk is reused
+// once the copy that last read it has completed.
+class PinnedPool {
+ public:
+  void upload(void* dst, const void* src, size_t n, cudaStream_t s) {
+    Chunk* c = nullptr;
+    {
+      std::lock_guard<std::mutex> g(mu_);
+      for (auto& ch : chunks_)
+        if (!ch->busy && ch->cap >= n && (!ch->recorded || cudaEventQuery(ch->ev) == cudaSuccess)) {
+          c = ch.get();
+          break;
+        }
+      if (!c) {
+        size_t cap = size_t(1) << 20;
+        while (cap < n) cap <<= 1;
+        auto ch = std::make_unique<Chunk>();
+        FTB_CUDA(cudaHostAlloc(&ch->p, cap, cudaHostAllocPortable));
+        FTB_CUDA(cudaEventCreateWithFlags(&ch->ev, cudaEventDisableTiming));
+        ch->cap = cap;
+        chunks_.push_back(std::move(ch));
+        c = chunks_.back().get();
+      }
+      c->busy = true;
+    }
+    std::memcpy(c->p, src, n);
+    cudaError_t e = cudaMemcpyAsync(dst, c->p, n, cudaMemcpyHostToDevice, s);
+    if (e == cudaSuccess) e = cudaEventRecord(c->ev, s);
+    {
+      std::lock_guard<std::mutex> g(mu_);
+      c->recorded = c->recorded || e == cudaSuccess;
+      c->busy = false;
+    }
+    if (e != cudaSuccess) throw cuda_error(std::string("table upload: ") + cudaGetErrorString(e));
+  }
+
+ private:
+  struct Chunk {
+    void* p = nullptr;
+    size_t cap = 0;
+    cudaEvent_t ev = nullptr;
+    bool busy = false, recorded = false;
+  };
+  std::mutex mu_;
+  std::vector<std::unique_ptr<Chunk>> chunks_;
+};
+static PinnedPool& pinned_pool(int dev) {
+  static PinnedPool pools[64];
+  return pools[dev & 63];
+}
+
 // Host image of one table allocation: sections appended at 128-B offsets.
 struct Blob {
   std::vector<uint8_t> bytes;
@@ -250,6 +307,9 @@ struct ExecImpl {
   unsigned long long* d_trace = nullptr;
   void* d_blob = nullptr;             // one pool allocation: every section above but the workspace
   int device = -1;
+  double encode_ms = 0.0;             // host time spent encoding TMA descriptors (FTB_PROFILE_CREATE)
+  cudaEvent_t ready = nullptr;        // the table's upload has landed (recorded on the upload stream)
+  bool ready_known = false;           // `ready` observed complete: launches need not wait for it
   // streams this table was launched on, each with the event recorded after
   // its last launch: destroy frees only after all of them (stream order)
   std::vector<std::pair<cudaStream_t, cudaEvent_t>> launched;
@@ -271,6 +331,10 @@ struct ExecImpl {
     try {
       rs = device_res(device).reclaim;
     } catch (...) {
+    }
+    if (ready) {
+      if (rs) cudaStreamWaitEvent(rs, ready, 0);  // never free a table whose upload is in flight
+      cudaEventDestroy(ready);
     }
     for (auto& se : launched) {
       if (rs) cudaStreamWaitEvent(rs, se.second, 0);
@@ -391,6 +455,7 @@ static void build(ExecImpl& ex, const ftb_gemm_desc* probs, const ftb_program* p
     ex.pack_depth.push_back(depth);
     ex.pack_rows.push_back(lrows);
     if (!ffma && encode) {
+      const auto te0 = std::chrono::steady_clock::now();
       // A: [batch][M][lda], K contiguous. B: [batch][N][ldb] (NK) or [batch][K][ldb] (KN).
       DevMaps m;
       std::memset(&m, 0, sizeof(m));
@@ -426,6 +491,7 @@ static void build(ExecImpl& ex, const ftb_gemm_desc* probs, const ftb_program* p
       m.epi.n = static_cast<int32_t>(d.N);
       m.epi.pad_ = 0;
       ex.maps.push_back(m);
+      ex.encode_ms += std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - te0).count();
     }
     ex.problems.push_back(P);
 
@@ -513,13 +579,19 @@ static void build(ExecImpl& ex, const ftb_gemm_desc* probs, const ftb_program* p
 static void upload(ExecImpl& I) {
   FTB_CUDA(cudaGetDevice(&I.device));
   const cudaStream_t us = device_res(I.device).upload;
-  // one pool allocation for the whole table, filled by one async copy on the
-  // private upload stream; create returns once that copy has landed (a wait
-  // on this stream only — kernels running on other streams are not waited for)
+  // one pool allocation for the whole table, filled by one async copy (from a
+  // pinned staging chunk) on the private upload stream; create does not wait
+  // for it — the first launch on a stream waits for `ready` on the device
+  // the table is ready on the device when `ready` (recorded on the upload
+  // stream after its copy) has fired; launches wait for it device-side
+  auto send = [&](Blob& b) {
+    pinned_pool(I.device).upload(I.d_blob, b.bytes.data(), b.bytes.size(), us);
+    FTB_CUDA(cudaEventCreateWithFlags(&I.ready, cudaEventDisableTiming));
+    FTB_CUDA(cudaEventRecord(I.ready, us));
+  };
   auto commit = [&](Blob& b) {
     FTB_CUDA(cudaMallocAsync(&I.d_blob, std::max<size_t>(b.bytes.size(), 128), us));
-    FTB_CUDA(cudaMemcpyAsync(I.d_blob, b.bytes.data(), b.bytes.size(), cudaMemcpyHostToDevice, us));
-    FTB_CUDA(cudaStreamSynchronize(us));
+    send(b);
   };
   auto at = [&](size_t off) { return static_cast<uint8_t*>(I.d_blob) + off; };
   if (I.work.empty() || I.info.kernel == 1) {
@@ -908,8 +980,7 @@ static void upload(ExecImpl& I) {
     if (!tw.empty()) std::memcpy(b.bytes.data() + ot, tw.data(), sizeof(TcWork) * tw.size());
     if (!pairs.empty()) std::memcpy(b.bytes.data() + oq, pairs.data(), sizeof(TcPair) * pairs.size());
     // split-K counters start at zero (the Blob is zero-filled) and re-arm themselves
-    FTB_CUDA(cudaMemcpyAsync(I.d_blob, b.bytes.data(), b.bytes.size(), cudaMemcpyHostToDevice, us));
-    FTB_CUDA(cudaStreamSynchronize(us));
+    send(b);
   }
   int sms = device_sms();
   if (sms <= 0) sms = 148;
@@ -961,9 +1032,19 @@ ftb_status ftb_exec_create(const ftb_gemm_desc* problems, const ftb_program* pro
     if (!out || !problems || !programs) throw ftb::input_error("null argument");
     auto* ex = new ftb_exec();
     try {
+      static const bool prof = std::getenv("FTB_PROFILE_CREATE") != nullptr;
+      auto t0 = std::chrono::steady_clock::now();
       ftb::build(ex->impl, problems, programs, n, /*encode=*/true);
+      auto t1 = std::chrono::steady_clock::now();
       auto& I = ex->impl;
       ftb::upload(I);
+      if (prof) {
+        auto t2 = std::chrono::steady_clock::now();
+        std::fprintf(stderr, "ftb_exec_create: %d problems, %lld items: build %.3f ms (encode %.3f ms), upload %.3f ms\n",
+                     n, static_cast<long long>(I.info.n_work),
+                     std::chrono::duration<double, std::milli>(t1 - t0).count(), I.encode_ms,
+                     std::chrono::duration<double, std::milli>(t2 - t1).count());
+      }
     } catch (...) {
       delete ex;
       throw;
@@ -990,6 +1071,15 @@ ftb_status ftb_exec_launch(ftb_exec* ex, void* stream) {
     // workspace): a launch on a new stream first waits for the previous one.
     // Captured launches are not tracked — a graph holding this table must not
     // outlive it (as with any buffer the graph references).
+    if (I.ready && !I.ready_known) {  // the table upload (create did not wait for it)
+      if (capturing) {
+        FTB_CUDA(cudaEventSynchronize(I.ready));  // a graph must not depend on an outside event
+        I.ready_known = true;
+      } else {
+        FTB_CUDA(cudaStreamWaitEvent(s, I.ready, 0));
+        I.ready_known = cudaEventQuery(I.ready) == cudaSuccess;
+      }
+    }
     if (!capturing && I.last_stream && I.last_stream != s)
       for (auto& se : I.launched)
         if (se.first == I.last_stream) FTB_CUDA(cudaStreamWaitEvent(s, se.second, 0));

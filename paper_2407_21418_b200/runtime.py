@@ -15,6 +15,7 @@ binding), the f-1 "persistent plan cache" of SURVEY.md §8.
 from __future__ import annotations
 
 import ctypes as C
+import functools
 import json
 import os
 import threading
@@ -34,8 +35,30 @@ from .mktune.workload import WorkloadInstance, bmm_spec, dense_spec, workload_ha
 CACHE_VERSION = 2
 
 
+@functools.lru_cache(maxsize=4096)
+def _dense_spec(N: int, K: int, hi: int, elem_bytes: int):
+    return dense_spec(N, K, (1, hi), elem_bytes)
+
+
+@functools.lru_cache(maxsize=4096)
+def _bmm_spec(b: int, i, j, k, elem_bytes: int, name: str):
+    return bmm_spec(b, i, j, k, elem_bytes=elem_bytes, name=name)
+
+
+def spec_hash(spec) -> str:
+    """workload_hash(spec), memoised on the (frozen) spec object: the runtime's
+    plan-cache key is computed per call, and the canonical-JSON hash costs
+    ~35 us (the specs of dense_instance / bmm_instance are memoised too, so a
+    dynamic-shape step's cache hits cost microseconds, not ~85 us each)."""
+    h = spec.__dict__.get("_ftb_hash")
+    if h is None:
+        h = workload_hash(spec)
+        object.__setattr__(spec, "_ftb_hash", h)
+    return h
+
+
 def dense_instance(M: int, N: int, K: int, elem_bytes: int = 2, m_max: int = 8192) -> WorkloadInstance:
-    return WorkloadInstance(dense_spec(N, K, (1, max(m_max, M)), elem_bytes), {"i": M})
+    return WorkloadInstance(_dense_spec(N, K, max(m_max, M), elem_bytes), {"i": M})
 
 
 def bmm_instance(b: int, M: int, N: int, K: int, dynamic=("i", "j"), elem_bytes: int = 2,
@@ -44,8 +67,8 @@ def bmm_instance(b: int, M: int, N: int, K: int, dynamic=("i", "j"), elem_bytes:
     (scores: i, j = T; context: i, k = T)."""
     ext = {"i": M, "j": N, "k": K}
     hi = max(t_max, M, N, K)
-    spec = bmm_spec(b, *[((1, hi) if a in dynamic else ext[a]) for a in ("i", "j", "k")], elem_bytes=elem_bytes,
-                    name="bmm-" + "".join(dynamic))
+    spec = _bmm_spec(b, *[((1, hi) if a in dynamic else ext[a]) for a in ("i", "j", "k")], elem_bytes,
+                     "bmm-" + "".join(dynamic))
     return WorkloadInstance(spec, {a: ext[a] for a in dynamic})
 
 
@@ -122,7 +145,7 @@ class Planner:
 
     def _key(self, inst: WorkloadInstance) -> tuple:
         c = self.coeffs
-        return (self.hw.name, self.hw.tcgen05_mode, (c.c0, c.c1, c.c2), workload_hash(inst.spec), inst.binding_key())
+        return (self.hw.name, self.hw.tcgen05_mode, (c.c0, c.c1, c.c2), spec_hash(inst.spec), inst.binding_key())
 
     def plan(self, instances: Sequence[WorkloadInstance]) -> list[PlanRecord]:
         """Top-1 program per instance (cached); misses are planned in one
