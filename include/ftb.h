@@ -71,13 +71,24 @@ typedef struct {
 /* ------------------------------------------------------------------------ */
 
 /* HardwareDescriptor (hardware.py:35-66): the 9 integer fields, plus the
- * B200 legality extension (0 = parity mode, exactly the reference). */
+ * B200 legality extension (0 = parity mode, exactly the reference). With
+ * legality = 1 the tile rules derive from the tcgen05 fields (0 = the sm_100a
+ * value): lane tiles are multiples of the largest MMA M atom (up to two
+ * slabs) or span a short axis; column tiles are the widest MMA N
+ * (mma_n_max, which a double-buffered accumulator must fit twice in
+ * tmem_columns) or span a short axis; reduce tiles are whole TMA swizzle
+ * atoms (tma_swizzle_bytes / elem_bytes elements). */
 typedef struct {
   int64_t num_cores, regs_per_core, smem_per_core_bytes;
   int64_t global_bw_bytes_per_s, shared_bw_bytes_per_s, peak_flops;
   int64_t default_active_blocks, active_blocks_per_core, align_elems;
   int32_t legality;   /* 0 = parity (reference), 1 = tcgen05 tile legality */
   int32_t reserved;
+  int64_t tmem_columns;       /* 512 */
+  int64_t mma_m_max;          /* 128: largest M of the cta_group::1 kind::f16 atoms */
+  int64_t mma_n_step;         /* 16  */
+  int64_t mma_n_max;          /* 256 */
+  int64_t tma_swizzle_bytes;  /* 128 */
 } ftb_hw;
 
 /* A bound WorkloadInstance (workload.py:187-220) flattened. Axis indices

@@ -117,6 +117,22 @@ Hw Hw::from_c(const ftb_hw& h) {
   for (int i = 0; i < 9; ++i)  // hardware.py:50-61
     if (v[i] <= 0) throw input_error(std::string("descriptor field '") + names[i] + "' must be strictly positive", names[i]);
   if (w.align & (w.align - 1)) throw input_error("descriptor field 'align_elems' must be a power of two", "align_elems");
+  if (w.legality) {
+    auto pick = [](int64_t v, int64_t dflt) { return v > 0 ? v : dflt; };
+    w.tmem_cols = pick(h.tmem_columns, 512);
+    w.m_max = pick(h.mma_m_max, 128);
+    w.n_step = pick(h.mma_n_step, 16);
+    w.n_max = pick(h.mma_n_max, 256);
+    w.swizzle = pick(h.tma_swizzle_bytes, 128);
+    if (w.m_max != 64 && w.m_max != 128) throw input_error("mma_m_atoms: the largest M must be 64 or 128", "mma_m_atoms");
+    if (w.n_step != 8 && w.n_step != 16) throw input_error("mma_n_step must be 8 or 16", "mma_n_step");
+    if (w.n_max < 2 * w.n_step || w.n_max > 256 || w.n_max % w.n_step)
+      throw input_error("mma_n_max must be a multiple of mma_n_step in [2 * step, 256]", "mma_n_max");
+    if (w.tmem_cols & (w.tmem_cols - 1) || w.tmem_cols < 2 * w.n_max || w.tmem_cols > 512)
+      throw input_error("tmem_columns must be a power of two in [2 * mma_n_max, 512]", "tmem_columns");
+    if (w.swizzle != 32 && w.swizzle != 64 && w.swizzle != 128)
+      throw input_error("tma_swizzle_bytes must be 32, 64 or 128", "tma_swizzle_bytes");
+  }
   return w;
 }
 
@@ -178,38 +194,46 @@ static std::vector<int64_t> reduce_options(int64_t e, int64_t align) {  // ukern
   return v;
 }
 
-bool tcgen05_legal(const Instance& in, const int64_t* smem, int relax_tau, int relax_level) {
+bool tcgen05_legal(const Instance& in, const Hw& hw, const int64_t* smem, int relax_tau, int relax_level) {
   // B200 extension: the uKernel's output tile must map onto efficient
-  // tcgen05 tiles in one of the two orientations: 128 or 256 TMEM lanes
-  // (M = 128 per MMA) x 256 accumulator columns (MMA N = 256); a tile spanning
-  // a whole short axis is also accepted. Measured on B200
-  // (scripts/micro/mma_bench.cu): a kind::f16 M=128 K=16 MMA costs ~100 clk
-  // whatever N <= 128 is (N=256: 128 clk), so narrower column tiles lose
-  // 25-70% of the tensor pipe; the C1 Dense step ran 1.59x faster with
-  // 256-column tiles (scripts/plan_variants.py). Batch tiles are free (one work
-  // item per batch entry); reduce tiles are whole 64-element TMA atoms.
+  // tcgen05 tiles in one of the two orientations — everything below derives
+  // from the descriptor's tcgen05 fields (sm_100a: M atoms up to 128 TMEM
+  // lanes, N up to 256 columns, 512 TMEM columns, 128-B TMA swizzle):
+  //   lanes  : whole MMA M slabs (m_max, or two of them), or a tile spanning
+  //            a short axis (<= m_max);
+  //   columns: the widest MMA N (n_max) — measured on B200
+  //            (scripts/micro/mma_bench.cu), an M=128 K=16 kind::f16 MMA costs
+  //            ~100 clk whatever N <= 128 is (N=256: 128 clk), so narrower
+  //            column tiles lose 25-70 % of the tensor pipe — or a whole short
+  //            axis; a column tile must also fit a double-buffered TMEM
+  //            accumulator (2 x tile <= tmem_columns);
+  //   reduce : whole TMA swizzle atoms (swizzle bytes / element bytes).
+  // Batch tiles are free (one work item per batch entry).
   if (in.ns < 2) return false;
   const int ai = in.ns - 2, aj = in.ns - 1;
   const int64_t ti = smem[ai], tj = smem[aj], Ei = in.ext[ai], Ej = in.ext[aj];
-  // lanes: full 128-lane MMA tiles (one or two), or one tile spanning a short axis
-  auto lane_ok = [](int64_t t, int64_t E) { return (t % 128 == 0 && t <= 256) || (t >= E && t <= 128); };
-  // columns: the full MMA N = 256, or a whole short axis
-  auto col_ok = [](int64_t t, int64_t E) { return t == 256 || (t >= E && t <= 256); };
+  const int64_t M = hw.m_max, N = std::min(hw.n_max, hw.tmem_cols / 2);
+  const int64_t k_atom = std::max<int64_t>(1, hw.swizzle / in.elem);
+  auto lane_ok = [M](int64_t t, int64_t E) { return (t % M == 0 && t <= 2 * M) || (t >= E && t <= M); };
+  auto col_ok = [N](int64_t t, int64_t E) { return t == N || (t >= E && t <= N); };
   for (int r = in.ns; r < in.na(); ++r)
-    if (smem[r] % 64) return false;
+    if (smem[r] % k_atom) return false;
   if (relax_tau == ai || relax_tau == aj) {
     const int64_t t_tau = relax_tau == ai ? ti : tj, t_o = relax_tau == ai ? tj : ti;
     const int64_t E_tau = relax_tau == ai ? Ei : Ej, E_o = relax_tau == ai ? Ej : Ei;
     if (relax_level == 1) {
       // first fallback rung: the main-axis tile may be any wide MMA N
-      // (multiple of 32 in [128, 256]) so that two parts can cover tau exactly;
-      // the other output axis stays strict in the matching role
-      auto col_wide = [](int64_t t, int64_t E) { return (t % 32 == 0 && t >= 128 && t <= 256) || (t >= E && t <= 256); };
+      // (multiple of 2 * n_step in [N / 2, N]) so that two parts can cover
+      // tau exactly; the other output axis stays strict in the matching role
+      const int64_t wstep = 2 * hw.n_step;
+      auto col_wide = [N, wstep](int64_t t, int64_t E) {
+        return (t % wstep == 0 && t >= N / 2 && t <= N) || (t >= E && t <= N);
+      };
       return (col_wide(t_tau, E_tau) && lane_ok(t_o, E_o)) || (lane_ok(t_tau, E_tau) && col_ok(t_o, E_o));
     }
-    // last fallback rung: the main-axis tile may take any size <= 256 (it is
+    // last fallback rung: the main-axis tile may take any size <= N (it is
     // padded inside the MMA tile); the other output axis stays strict
-    return t_tau <= 256 && (lane_ok(t_o, E_o) || col_ok(t_o, E_o));
+    return t_tau <= N && (lane_ok(t_o, E_o) || col_ok(t_o, E_o));
   }
   return (lane_ok(ti, Ei) && col_ok(tj, Ej)) || (lane_ok(tj, Ej) && col_ok(ti, Ei));
 }
@@ -305,7 +329,7 @@ Cands enumerate_legal(const Instance& in, const Hw& hw, int64_t cap, bool* trunc
   if (hw.legality) {  // B200 extension, applied right after enumeration + cap truncation
     std::vector<int64_t> keep;
     for (size_t i = 0; i < all.size(); ++i)
-      if (tcgen05_legal(in, all.smem_row(i), hw.relax_tau, hw.relax_level)) keep.push_back(static_cast<int64_t>(i));
+      if (tcgen05_legal(in, hw, all.smem_row(i), hw.relax_tau, hw.relax_level)) keep.push_back(static_cast<int64_t>(i));
     subset_inplace(all, keep);
   }
   return all;

@@ -46,7 +46,9 @@ struct Hw {
   int64_t cores, regs, smem, bw_g, bw_s, peak, zeta, active, align;
   int legality;       // 0 parity, 1 tcgen05 legality (B200 mode)
   int relax_tau = -1; // B200 fallback: space axis whose tile is relaxed
-  int relax_level = 2; // 1: tau tile may be any multiple of 32 in [128, 256] as MMA N; 2: any size <= 256
+  int relax_level = 2; // 1: tau tile may be any wide MMA N (multiple of 2 * n_step in [n_max / 2, n_max]); 2: any size <= n_max
+  // tcgen05 legality parameters (ftb_hw; the sm_100a values by default)
+  int64_t tmem_cols = 512, m_max = 128, n_step = 16, n_max = 256, swizzle = 128;
   static Hw from_c(const ftb_hw& h);
 };
 
@@ -104,7 +106,7 @@ std::vector<PlanRow> pool_export(const Cands& c, int tau);
 std::vector<std::pair<PlanRow, double>> rank_topk(const Cands& c, int tau, const ftb_coeffs& co,
                                                   int k, bool normalize);
 // B200 legality predicate (extension; parity mode never calls it).
-bool tcgen05_legal(const Instance& in, const int64_t* smem, int relax_tau = -1, int relax_level = 2);
+bool tcgen05_legal(const Instance& in, const Hw& hw, const int64_t* smem, int relax_tau = -1, int relax_level = 2);
 
 }  // namespace plan
 }  // namespace ftb

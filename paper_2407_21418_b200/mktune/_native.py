@@ -20,7 +20,8 @@ class Hw(C.Structure):
     _fields_ = [(f, C.c_int64) for f in (
         "num_cores", "regs_per_core", "smem_per_core_bytes", "global_bw_bytes_per_s",
         "shared_bw_bytes_per_s", "peak_flops", "default_active_blocks", "active_blocks_per_core", "align_elems",
-    )] + [("legality", C.c_int32), ("reserved", C.c_int32)]
+    )] + [("legality", C.c_int32), ("reserved", C.c_int32)] + [(f, C.c_int64) for f in (
+        "tmem_columns", "mma_m_max", "mma_n_step", "mma_n_max", "tma_swizzle_bytes")]
 
 
 class Inst(C.Structure):
@@ -93,6 +94,12 @@ def hw_struct(hw) -> Hw:
     for f, _ in Hw._fields_[:9]:
         setattr(h, f, int(getattr(hw, f)))
     h.legality = 1 if getattr(hw, "tmem_columns", None) is not None else 0
+    if h.legality:  # the tile rules derive from these (planner.cpp tcgen05_legal)
+        h.tmem_columns = int(hw.tmem_columns)
+        h.mma_m_max = int(max(hw.mma_m_atoms))
+        h.mma_n_step = int(hw.mma_n_step)
+        h.mma_n_max = int(hw.mma_n_max)
+        h.tma_swizzle_bytes = int(hw.tma_swizzle_bytes)
     return h
 
 

@@ -27,7 +27,9 @@ INT_FIELDS = (
     "active_blocks_per_core",
     "align_elems",
 )
-# sm_100a extension fields: (name, the only value the executor supports)
+# sm_100a extension fields and their sm_100a values (b200_bf16(tcgen05=True));
+# other values re-parameterise the legality rules (planner.cpp tcgen05_legal)
+# within what the executor can run (validated below)
 EXT_FIELDS = {
     "tmem_columns": 512,
     "mma_m_atoms": (64, 128),
@@ -76,11 +78,33 @@ class HardwareDescriptor:
         if set_ext and len(set_ext) != len(EXT_FIELDS):
             missing = [k for k in EXT_FIELDS if getattr(self, k) is None][0]
             raise InputError(f"tcgen05 extension field '{missing}' is missing", field=missing)
-        for k in set_ext:
-            if getattr(self, k) != EXT_FIELDS[k]:
-                raise InputError(
-                    f"tcgen05 extension field '{k}' must be {EXT_FIELDS[k]!r} on sm_100a", field=k
-                )
+        if set_ext:
+            self._check_tcgen05()
+
+    def _check_tcgen05(self) -> None:
+        """The executor's limits on the tcgen05 fields (sm_100a kind::f16,
+        cta_group::1): M atoms from {64, 128}; N step 8 or 16; widest N a
+        multiple of the step up to 256; TMEM a power of two holding two
+        widest accumulators, at most 512 columns; a 32/64/128-B swizzle."""
+        atoms = self.mma_m_atoms
+        if not isinstance(atoms, tuple) or not atoms or any(a not in (64, 128) for a in atoms):
+            raise InputError("tcgen05 extension field 'mma_m_atoms' must be a non-empty subset of (64, 128)",
+                             field="mma_m_atoms")
+        step, nmax, cols, swz = self.mma_n_step, self.mma_n_max, self.tmem_columns, self.tma_swizzle_bytes
+        for k, v in (("mma_n_step", step), ("mma_n_max", nmax), ("tmem_columns", cols), ("tma_swizzle_bytes", swz)):
+            if isinstance(v, bool) or not isinstance(v, int) or v <= 0:
+                raise InputError(f"tcgen05 extension field '{k}' must be a positive integer", field=k)
+        if step not in (8, 16):
+            raise InputError("tcgen05 extension field 'mma_n_step' must be 8 or 16", field="mma_n_step")
+        if nmax % step or not 2 * step <= nmax <= 256:
+            raise InputError("tcgen05 extension field 'mma_n_max' must be a multiple of mma_n_step in [2*step, 256]",
+                             field="mma_n_max")
+        if cols & (cols - 1) or not 2 * nmax <= cols <= 512:
+            raise InputError("tcgen05 extension field 'tmem_columns' must be a power of two in [2*mma_n_max, 512]",
+                             field="tmem_columns")
+        if swz not in (32, 64, 128):
+            raise InputError("tcgen05 extension field 'tma_swizzle_bytes' must be 32, 64 or 128",
+                             field="tma_swizzle_bytes")
 
     @property
     def total_active_blocks(self) -> int:

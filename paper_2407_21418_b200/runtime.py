@@ -32,7 +32,7 @@ from .mktune.hardware import HardwareDescriptor, b200_bf16, b200_ffma
 from .mktune.scoring import SiaCoeffs
 from .mktune.workload import WorkloadInstance, bmm_spec, dense_spec, workload_hash
 
-CACHE_VERSION = 2
+CACHE_VERSION = 3
 
 
 @functools.lru_cache(maxsize=4096)
@@ -138,6 +138,8 @@ class Planner:
         self.coeffs = coeffs or SiaCoeffs()
         self.threads = threads
         self.native_cover = os.environ.get("FTB_NATIVE_COVER", "1") != "0"
+        # the whole descriptor (name + every field, tcgen05 ones included) keys the cache
+        self._hw_key = json.dumps(self.hw.to_doc(), sort_keys=True)
         self._cache: dict[tuple, PlanRecord] = {}
         self._exe_cache: dict[tuple, Executable] = {}  # insertion-ordered LRU of lowered tables
         self.exe_cache_size = 32
@@ -145,7 +147,7 @@ class Planner:
 
     def _key(self, inst: WorkloadInstance) -> tuple:
         c = self.coeffs
-        return (self.hw.name, self.hw.tcgen05_mode, (c.c0, c.c1, c.c2), spec_hash(inst.spec), inst.binding_key())
+        return (self._hw_key, (c.c0, c.c1, c.c2), spec_hash(inst.spec), inst.binding_key())
 
     def plan(self, instances: Sequence[WorkloadInstance]) -> list[PlanRecord]:
         """Top-1 program per instance (cached); misses are planned in one

@@ -97,3 +97,62 @@ def test_descriptor_roundtrip_and_errors():
     assert e.value.field == "bogus"
     with pytest.raises(errors.InputError):
         hardware.load_hardware_descriptor({**doc, "align_elems": 48})
+
+
+def test_legality_derives_from_the_tcgen05_descriptor():
+    """the B200 legality rules come from the descriptor's
+    tcgen05 fields, not constants. With mma_n_max = 128 (and 256 TMEM
+    columns) the widest column tile is 128: every plan's output tiles are
+    whole 128-lane slabs / 128-column MMA tiles or span a short axis, and the
+    256-column plans of the sm_100a descriptor disappear. A 64-B swizzle
+    makes 32-element reduce tiles legal; invalid values are InputErrors."""
+    import dataclasses
+
+    import pytest
+
+    from paper_2407_21418_b200.mktune.errors import InputError
+    from paper_2407_21418_b200.mktune.hardware import b200_bf16
+    from paper_2407_21418_b200.runtime import Planner, bmm_instance, dense_instance
+
+    base = b200_bf16(tcgen05=True)
+    narrow = dataclasses.replace(base, mma_n_max=128, tmem_columns=256)
+    shapes = [dense_instance(1216, 2304, 768), dense_instance(4096, 768, 768), dense_instance(160, 3072, 768),
+              bmm_instance(384, 100, 100, 64)]
+
+    def out_tiles(hw):
+        recs = Planner(hw=hw).plan(shapes)
+        res = []
+        for inst, r in zip(shapes, recs):
+            g = r.program
+            ns = g.n_space
+            res.append([(int(g.smem[p][ns - 2]), int(g.smem[p][ns - 1])) for p in range(g.n_parts)])
+        return res, recs
+
+    wide, _ = out_tiles(base)
+    slim, recs = out_tiles(narrow)
+    assert any(256 in t for tiles in wide for t in tiles), "the sm_100a descriptor picks 256-column tiles"
+    assert all(max(t) <= 256 for tiles in slim for t in tiles)
+    for inst, tiles, r in zip(shapes, slim, recs):
+        ext = [inst.extents[a] for a in inst.spec.space_axes][-2:]
+        for ti, tj in tiles:
+            ok = lambda lane, col, El, Ec: (((lane % 128 == 0 and lane <= 256) or (El <= lane <= 128))  # noqa: E731
+                                             and (col == 128 or Ec <= col <= 128))
+            if r.stage < 4:  # strict rung: the narrowed rule holds in one of the two orientations
+                assert ok(ti, tj, ext[0], ext[1]) or ok(tj, ti, ext[1], ext[0]), (inst.extents, ti, tj)
+    assert slim != wide
+    with pytest.raises(InputError):
+        dataclasses.replace(base, mma_n_max=384)
+    with pytest.raises(InputError):
+        dataclasses.replace(base, tmem_columns=256)  # cannot hold two 256-column accumulators
+    with pytest.raises(InputError):
+        dataclasses.replace(base, mma_m_atoms=(96,))
+    # with a 32-element alignment, a 128-B swizzle still demands 64-element
+    # reduce tiles (one bf16 swizzle atom); a 64-B swizzle admits 32
+    a32 = dataclasses.replace(base, align_elems=32)
+    swz64 = dataclasses.replace(a32, tma_swizzle_bytes=64)
+    from paper_2407_21418_b200.mktune.ukernel import enumerate_ukernels
+
+    inst = dense_instance(160, 768, 768)
+    ks_default = {int(k) for k in enumerate_ukernels(inst, a32).smem[:, 2]}
+    ks_64 = {int(k) for k in enumerate_ukernels(inst, swz64).smem[:, 2]}
+    assert all(k % 64 == 0 for k in ks_default) and any(k % 64 for k in ks_64)
