@@ -125,7 +125,10 @@ def lib() -> C.CDLL:
         "ftb_exec_get_config": (i32, [vp, C.POINTER(i32)]),
         "ftb_test_occupy_sms": (i32, [i32, vp, i64, vp]),
     }
+    optional = {"ftb_test_occupy_sms"}  # test hook: absent from older builds used in A/B runs
     for name, (res, args) in sig.items():
+        if name in optional and not hasattr(L, name):
+            continue
         fn = getattr(L, name)
         fn.restype = res
         fn.argtypes = args

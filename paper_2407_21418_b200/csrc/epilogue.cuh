@@ -68,12 +68,12 @@ __device__ __forceinline__ void store_rows8(const float* tb, int rl, int r, int 
     if (f32) {
       float* dst = static_cast<float*>(C) + off;
       if (n == 8 && ((reinterpret_cast<uintptr_t>(dst) & 15u) == 0)) {
-        reinterpret_cast<float4*>(dst)[0] = make_float4(e[0], e[1], e[2], e[3]);
-        reinterpret_cast<float4*>(dst)[1] = make_float4(e[4], e[5], e[6], e[7]);
+        __stcg(reinterpret_cast<float4*>(dst), make_float4(e[0], e[1], e[2], e[3]));  // st.global: C is device memory
+        __stcg(reinterpret_cast<float4*>(dst) + 1, make_float4(e[4], e[5], e[6], e[7]));
       } else {
 #pragma unroll
         for (int q = 0; q < 8; ++q)
-          if (q < n) dst[q] = e[q];
+          if (q < n) __stcg(dst + q, e[q]);
       }
     } else {
       __nv_bfloat16* dst = static_cast<__nv_bfloat16*>(C) + off;
@@ -85,11 +85,11 @@ __device__ __forceinline__ void store_rows8(const float* tb, int rl, int r, int 
           __nv_bfloat162 h = __floats2bfloat162_rn(e[2 * q], e[2 * q + 1]);
           pw[q] = *reinterpret_cast<uint32_t*>(&h);
         }
-        *reinterpret_cast<uint4*>(dst) = pk;
+        __stcg(reinterpret_cast<uint4*>(dst), pk);
       } else {
 #pragma unroll
         for (int q = 0; q < 8; ++q)
-          if (q < n) dst[q] = __float2bfloat16_rn(e[q]);
+          if (q < n) __stcg(reinterpret_cast<unsigned short*>(dst) + q, __bfloat16_as_ushort(__float2bfloat16_rn(e[q])));
       }
     }
   }

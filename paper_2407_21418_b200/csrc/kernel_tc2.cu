@@ -56,8 +56,11 @@ template <int S>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kTcThreads, 1)
     ftb_tc2_kernel(const TcPair* __restrict__ work, int32_t n_work, TcConfig cfg) {
   extern __shared__ uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
-                                             ~static_cast<uintptr_t>(1023));
+  // 1024-B aligned base, derived by pointer arithmetic on the __shared__ array
+  // so the compiler keeps the shared state space: every staging / transpose
+  // access below compiles to STS/LDS rather than generic ST.E/LD.E (an
+  // integer round trip through uintptr_t made all 1000 of them generic)
+  uint8_t* smem = smem_raw + ((1024u - (smem_addr(smem_raw) & 1023u)) & 1023u);
   uint8_t* lane_buf = smem;                                   // S x 16 KiB
   uint8_t* col_buf = smem + S * kLaneStageBytes;              // S x col_stage_bytes (N/2 rows)
   float* epi_buf = reinterpret_cast<float*>(col_buf + S * cfg.col_stage_bytes);

@@ -22,7 +22,8 @@ for spec in os.environ.get("SHAPES", "dense 128 256 64;dense 608 768 768;bmm 384
         Np = (N + 7) // 8 * 8
 
         def mk():
-            A = (torch.rand(b, M, K, device="cuda") * 2 - 1).bfloat16()
+            Kp = (K + 7) // 8 * 8
+            A = (torch.rand(b, M, Kp, device="cuda") * 2 - 1).bfloat16()[:, :, :K]
             B = ((torch.rand(b, N, K, device="cuda") if lay == "nk" else torch.rand(b, K, N, device="cuda")) * 2 - 1).bfloat16()
             C = torch.empty(b, M, Np, device="cuda", dtype=torch.bfloat16)[:, :, :N]
             return A, B, C
