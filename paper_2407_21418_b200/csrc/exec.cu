@@ -955,8 +955,14 @@ static void upload(ExecImpl& I) {
     // every item short (a mixed table such as the C1 step keeps its ring
     // stages for the long Dense items: measured 0.80 vs 0.83 ms with eight warps)
     bool e8 = !pairing && !split && n > sms_here && kb_max <= 8 && out_bytes < (int64_t(48) << 10) * n;
-    if (env_e8) e8 = env_e8[0] == '1' && !pairing && !split;
-    I.cfg.epi8 = e8 ? 1 : 0;
+    int mode = e8 ? 1 : 0;
+    // Column split (mode 2, OPT-IN FTB_EPI8=2): both warp groups drain half
+    // of every item's columns. Measured on tables of <= one item per CTA it
+    // LOSES (C1 out M=608 6.39 -> 6.65 us, qkv M=1472 9.2 -> 9.7 us,
+    // profiles/r2ab_epi8_colsplit.txt): the 320-thread kernel's smaller ring
+    // and register budget cost more than the shorter epilogue tail saves.
+    if (env_e8) mode = (env_e8[0] == '1' || env_e8[0] == '2') && !pairing && !split ? env_e8[0] - '0' : 0;
+    I.cfg.epi8 = mode;
   }
   I.n_singles = static_cast<int64_t>(tw.size());
   I.n_pairs = static_cast<int64_t>(pairs.size());

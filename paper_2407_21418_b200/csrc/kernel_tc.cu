@@ -325,7 +325,7 @@ __global__ void __launch_bounds__(kEpi8 ? 384 : kTcThreads, 1)
     }
     for (int a = 0; a < cfg.n_acc; ++a) {
       mbar_init(&tfull[a], 1);
-      mbar_init(&tempty[a], 4);  // one arrive per epilogue warp
+      mbar_init(&tempty[a], (kEpi8 && cfg.epi8 == 2) ? 8 : 4);  // one arrive per epilogue warp on the slot
     }
     fence_barrier_init();
   }
@@ -593,15 +593,19 @@ __global__ void __launch_bounds__(kEpi8 ? 384 : kTcThreads, 1)
     // kEpi8: two groups of four warps take alternate items (alternate TMEM
     // slots), 8 KiB each (the staging doubles; the ring gives up stages), so
     // two items' epilogues run concurrently.
+    // cfg.epi8 == 2 (column split): both groups take EVERY item, each half
+    // of its columns — for tables of at most one item per CTA, where the
+    // item's epilogue is the launch's tail and halving it shortens the launch.
     const int egrp = kEpi8 ? (warp - 2) >> 2 : 0;
+    const bool csplit = kEpi8 && cfg.epi8 == 2;
     uint8_t* region = reinterpret_cast<uint8_t*>(epi_buf) + (kEpi8 ? (warp - 2) : quad) * kEpiWarpBytes;
-    const int step = kEpi8 ? 2 : 1;
-    uint32_t local = egrp, ngrp = 0;
+    const int step = (kEpi8 && !csplit) ? 2 : 1;
+    uint32_t local = csplit ? 0 : egrp, ngrp = 0;
 #ifdef FTB_PROD_PROFILE
     unsigned long long e_wait = 0, e_t0 = clock64();
 #endif
     TcWork nxt;
-    const int w0 = static_cast<int>(blockIdx.x) + egrp * G;
+    const int w0 = static_cast<int>(blockIdx.x) + (csplit ? 0 : egrp * G);
     if (w0 < n_work) nxt = load_work(work, w0);
     for (int w = w0; w < n_work; w += step * G, local += step) {
       const TcWork it = nxt;
@@ -626,20 +630,30 @@ __global__ void __launch_bounds__(kEpi8 ? 384 : kTcThreads, 1)
         __syncwarp();
         if (lane == 0) mbar_arrive(&tempty[slot]);
       };
+      // this warp group's TMEM / C column window (the whole item unless csplit;
+      // the cut sits on a 32-column store-box boundary)
+      int clo = 0, clen = it.col_len;
+      if (csplit) {
+        const int half = ((it.col_len + 1) / 2 + 31) & ~31;
+        clo = egrp * half;
+        clen = min(it.col_len, clo + half) - clo;
+      }
       if (it.flags & kFlagSplitK) {
         split_epilogue<kCluster>(cfg, it, region, taddr, lane_base, swap, f32, release, reinterpret_cast<float*>(smem));
+      } else if (clen <= 0) {
+        release();
       } else if (!it.pack) {
-        epilogue_tile(region, ngrp, taddr, lane_base < it.lane_len, tma, swap, f32, &it.maps->out, it.C, it.ldc,
-                      it.lane0, it.lane_len, lane_base, it.col0, it.col_len, it.batch, release,
+        epilogue_tile(region, ngrp, taddr + clo, lane_base < it.lane_len, tma, swap, f32, &it.maps->out, it.C, it.ldc,
+                      it.lane0, it.lane_len, lane_base, it.col0 + clo, clen, it.batch, release,
                       (it.flags & kFlagEpiOp) ? &it.maps->epi : nullptr);
       } else {
         // block-diagonal pack: this warp's lane quadrant belongs to entry e
         const int wpe = pack_lane_rows(it.pack) / 32;  // warps per entry
         const int e = quad / wpe, r0 = (quad % wpe) * 32;
         const bool active = e < pack_nb(it.pack) && r0 < it.lane_len;
-        epilogue_tile(region, ngrp, taddr + e * 64, active, tma, swap, f32, &it.maps->out,
+        epilogue_tile(region, ngrp, taddr + e * 64 + clo, active, tma, swap, f32, &it.maps->out,
                       static_cast<char*>(it.C) + static_cast<size_t>(e) * it.c_bs * (f32 ? 4 : 2), it.ldc, 0,
-                      it.lane_len, r0, 0, it.col_len, it.batch + e, release);
+                      it.lane_len, r0, clo, clen, it.batch + e, release);
       }
       if (quad == 0 && lane == 0) trace_ev(cfg, local, 5);
     }
