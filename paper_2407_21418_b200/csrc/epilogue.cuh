@@ -22,11 +22,11 @@ __device__ __forceinline__ void store_row32(void* C, int64_t off, const float* v
     if (vec_ok && n == 32) {
 #pragma unroll
       for (int q = 0; q < 8; ++q)
-        reinterpret_cast<float4*>(dst)[q] = make_float4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
+        __stcg(reinterpret_cast<float4*>(dst) + q, make_float4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]));
     } else {
 #pragma unroll
       for (int e = 0; e < 32; ++e)
-        if (e < n) dst[e] = v[e];
+        if (e < n) __stcg(dst + e, v[e]);
     }
   } else {
     __nv_bfloat16* dst = static_cast<__nv_bfloat16*>(C) + off;
@@ -40,12 +40,12 @@ __device__ __forceinline__ void store_row32(void* C, int64_t off, const float* v
           __nv_bfloat162 h = __floats2bfloat162_rn(v[q * 8 + 2 * e], v[q * 8 + 2 * e + 1]);
           pw[e] = *reinterpret_cast<uint32_t*>(&h);
         }
-        reinterpret_cast<uint4*>(dst)[q] = pk;
+        __stcg(reinterpret_cast<uint4*>(dst) + q, pk);
       }
     } else {
 #pragma unroll
       for (int e = 0; e < 32; ++e)
-        if (e < n) dst[e] = __float2bfloat16_rn(v[e]);
+        if (e < n) __stcg(reinterpret_cast<unsigned short*>(dst) + e, __bfloat16_as_ushort(__float2bfloat16_rn(v[e])));
     }
   }
 }
