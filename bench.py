@@ -225,16 +225,24 @@ def run_reference(args, rank, world):
 
 
 def lib_sha() -> str:
+    """sha256 (16 hex) over the kernel / executor sources and their build
+    flags: identifies the build an ncu artefact was measured on even when the
+    driver rebuilds libftb.so from the same sources."""
     import hashlib
 
-    p = ROOT / "paper_2407_21418_b200" / "libftb.so"
-    return hashlib.sha256(p.read_bytes()).hexdigest()[:16] if p.exists() else ""
+    h = hashlib.sha256()
+    csrc = ROOT / "paper_2407_21418_b200" / "csrc"
+    for f in sorted(csrc.glob("*")):
+        if f.suffix in (".cu", ".cuh", ".h", ".cpp") or f.name == "Makefile":
+            h.update(f.name.encode())
+            h.update(f.read_bytes())
+    return h.hexdigest()[:16]
 
 
 def load_traffic(tag: str):
     """Per-launch DRAM bytes of the dominant kernel from the ncu artefact
-    (scripts/ncu_traffic.py), used only when it was measured on THIS build
-    of libftb.so (sha256 prefix) — otherwise null with the reason."""
+    (scripts/ncu_shapes.py), used only when it was measured on THIS build
+    (sha256 of the kernel sources) — otherwise null with the reason."""
     p = ROOT / "profiles" / "ncu_traffic.json"
     if not p.exists():
         return None, "no ncu artefact"
@@ -245,7 +253,7 @@ def load_traffic(tag: str):
     if not isinstance(d, dict):
         return None, f"no per-build '{tag}' entry in the ncu artefact"
     if d.get("lib_sha") != lib_sha():
-        return None, f"ncu artefact is for libftb.so {d.get('lib_sha')}, this build is {lib_sha()}"
+        return None, f"ncu artefact is for sources {d.get('lib_sha')}, this build is {lib_sha()}"
     return d.get("dram_bytes_per_launch"), "ncu dram__bytes_read.sum + dram__bytes_write.sum, " + d.get("how", "")
 
 

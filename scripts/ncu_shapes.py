@@ -130,8 +130,9 @@ def report(csv_path, manifest, tag):
                      "tensor_pct": m.get("sm__pipe_tensor_cycles_active.avg.pct_of_peak_sustained_elapsed"),
                      "l2_hit_pct": m.get("lts__t_sector_hit_rate.pct"), "sm_ghz": m.get("sm__cycles_elapsed.avg.per_second"),
                      "top_stalls": [(s, round(v, 2)) for v, s in stalls[:3]], "kernel": m["kernel"][:60]})
-    lib = ROOT / "paper_2407_21418_b200" / "libftb.so"
-    sha = hashlib.sha256(lib.read_bytes()).hexdigest()[:16] if lib.exists() else ""
+    from bench import lib_sha  # the same source hash bench.py checks
+
+    sha = lib_sha()
     c1 = [r for r in rows if r["cfg"] == "c1"]
     step = next(r for r in rows if r["cfg"] == "c1_step")
     traffic = {
