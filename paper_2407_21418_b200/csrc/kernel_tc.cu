@@ -227,35 +227,56 @@ __device__ __forceinline__ void cluster_reduce(const TcConfig& cfg, const TcWork
 #pragma unroll
     for (int e = 0; e < 32; ++e) v[e] = 0.f;
     const uint32_t mine = smem_addr(csmem + (static_cast<size_t>(ch * 4 + quad) << 10) + lane * 4);
-    int p = 0;
-    for (; p + 2 <= s; p += 2) {
-      const uint32_t pa = mapa_shared(mine, static_cast<uint32_t>(p));
-      const uint32_t pb = mapa_shared(mine, static_cast<uint32_t>(p + 1));
-      float4 a[8], b[8];
+    if (s == 4) {
+      // all four peers' loads in flight at once (one DSMEM round trip), then
+      // the fixed-order sum
+      float4 a[4][8];
 #pragma unroll
-      for (int g = 0; g < 8; ++g) {
-        a[g] = ld_dsmem_v4(pa + g * 512);
-        b[g] = ld_dsmem_v4(pb + g * 512);
+      for (int p = 0; p < 4; ++p) {
+        const uint32_t pa = mapa_shared(mine, static_cast<uint32_t>(p));
+#pragma unroll
+        for (int g = 0; g < 8; ++g) a[p][g] = ld_dsmem_v4(pa + g * 512);
       }
 #pragma unroll
-      for (int g = 0; g < 8; ++g) {
-        v[4 * g] = (v[4 * g] + a[g].x) + b[g].x;
-        v[4 * g + 1] = (v[4 * g + 1] + a[g].y) + b[g].y;
-        v[4 * g + 2] = (v[4 * g + 2] + a[g].z) + b[g].z;
-        v[4 * g + 3] = (v[4 * g + 3] + a[g].w) + b[g].w;
+      for (int p = 0; p < 4; ++p)
+#pragma unroll
+        for (int g = 0; g < 8; ++g) {
+          v[4 * g] += a[p][g].x;
+          v[4 * g + 1] += a[p][g].y;
+          v[4 * g + 2] += a[p][g].z;
+          v[4 * g + 3] += a[p][g].w;
+        }
+    } else {
+      int p = 0;
+      for (; p + 2 <= s; p += 2) {
+        const uint32_t pa = mapa_shared(mine, static_cast<uint32_t>(p));
+        const uint32_t pb = mapa_shared(mine, static_cast<uint32_t>(p + 1));
+        float4 a[8], b[8];
+#pragma unroll
+        for (int g = 0; g < 8; ++g) {
+          a[g] = ld_dsmem_v4(pa + g * 512);
+          b[g] = ld_dsmem_v4(pb + g * 512);
+        }
+#pragma unroll
+        for (int g = 0; g < 8; ++g) {
+          v[4 * g] = (v[4 * g] + a[g].x) + b[g].x;
+          v[4 * g + 1] = (v[4 * g + 1] + a[g].y) + b[g].y;
+          v[4 * g + 2] = (v[4 * g + 2] + a[g].z) + b[g].z;
+          v[4 * g + 3] = (v[4 * g + 3] + a[g].w) + b[g].w;
+        }
       }
-    }
-    if (p < s) {
-      const uint32_t pa = mapa_shared(mine, static_cast<uint32_t>(p));
-      float4 a[8];
+      if (p < s) {
+        const uint32_t pa = mapa_shared(mine, static_cast<uint32_t>(p));
+        float4 a[8];
 #pragma unroll
-      for (int g = 0; g < 8; ++g) a[g] = ld_dsmem_v4(pa + g * 512);
+        for (int g = 0; g < 8; ++g) a[g] = ld_dsmem_v4(pa + g * 512);
 #pragma unroll
-      for (int g = 0; g < 8; ++g) {
-        v[4 * g] += a[g].x;
-        v[4 * g + 1] += a[g].y;
-        v[4 * g + 2] += a[g].z;
-        v[4 * g + 3] += a[g].w;
+        for (int g = 0; g < 8; ++g) {
+          v[4 * g] += a[g].x;
+          v[4 * g + 1] += a[g].y;
+          v[4 * g + 2] += a[g].z;
+          v[4 * g + 3] += a[g].w;
+        }
       }
     }
     const int c0 = ch * 32;
@@ -671,21 +692,21 @@ __global__ void __launch_bounds__(kEpi8 ? 384 : kTcThreads, 1)
   __syncthreads();
   if (kCluster) {  // one item per CTA: reduce the cluster's split-K partials on chip
 #ifdef FTB_TRACE
-    if (threadIdx.x == 64) trace_kb(cfg, 60, 0);  // debug: before the first cluster barrier
+    if (threadIdx.x == 64 && cfg.trace) cfg.trace[blockIdx.x * kTracePerCta + kTraceItems * kTraceEvents + 120] = clock64();  // debug (clk): before the first cluster barrier
 #endif
     cluster_sync();              // every split's partial written (release / acquire at cluster scope)
 #ifdef FTB_TRACE
-    if (threadIdx.x == 64) trace_kb(cfg, 60, 1);
+    if (threadIdx.x == 64 && cfg.trace) cfg.trace[blockIdx.x * kTracePerCta + kTraceItems * kTraceEvents + 121] = clock64();
 #endif
     if (warp >= 2 && static_cast<int>(blockIdx.x) < n_work)
       cluster_reduce(cfg, load_work(work, blockIdx.x), reinterpret_cast<uint8_t*>(epi_buf) + (warp & 3) * kEpiWarpBytes,
                      reinterpret_cast<float*>(smem), warp & 3);
 #ifdef FTB_TRACE
-    if (threadIdx.x == 64) trace_kb(cfg, 61, 0);  // debug: warp 2 done reducing
+    if (threadIdx.x == 64 && cfg.trace) cfg.trace[blockIdx.x * kTracePerCta + kTraceItems * kTraceEvents + 122] = clock64();  // debug (clk): warp 2 done reducing
 #endif
     cluster_sync();              // peers have read this CTA's partial before it exits
 #ifdef FTB_TRACE
-    if (threadIdx.x == 64) trace_kb(cfg, 61, 1);
+    if (threadIdx.x == 64 && cfg.trace) cfg.trace[blockIdx.x * kTracePerCta + kTraceItems * kTraceEvents + 123] = clock64();
 #endif
   }
 #ifdef FTB_TRACE

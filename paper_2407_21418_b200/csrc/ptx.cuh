@@ -284,8 +284,10 @@ __device__ __forceinline__ float ld_dsmem_f32(uint32_t addr) {
 // 16-byte load from a peer CTA's shared memory
 __device__ __forceinline__ float4 ld_dsmem_v4(uint32_t addr) {
   float4 v;
-  asm volatile("ld.shared::cluster.v4.f32 {%0, %1, %2, %3}, [%4];" : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "r"(addr)
-               : "memory");
+  // not volatile / no memory clobber: the partials are published before a
+  // cluster barrier and never change afterwards, so the compiler may batch
+  // and reorder these loads freely
+  asm("ld.shared::cluster.v4.f32 {%0, %1, %2, %3}, [%4];" : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "r"(addr));
   return v;
 }
 __device__ __forceinline__ void cluster_sync() {

@@ -93,10 +93,11 @@ for spec in os.environ.get("SHAPES", "bmm 384 5 5 64 nk;bmm 384 100 100 64 nk;de
               f"commit {np.median(r[:, 0, 3]):6.2f} epi {np.median(r[:, 0, 4]):6.2f} rel {np.median(r[:, 0, 5]):6.2f} "
               f"end p50 {np.median(en):6.2f} max {en.max():6.2f}{gap}")
         prev_end = en.max()
-        if os.environ.get("CL"):
-            kbr = np.where(kb > 0, kb.astype(np.int64) - t0, -1) / 1e3
-            print(f"     cluster: before sync1 p50 {np.median(kbr[:, 60, 0]):.2f} after sync1 {np.median(kbr[:, 60, 1]):.2f} "
-                  f"reduced {np.median(kbr[:, 61, 0]):.2f} after sync2 {np.median(kbr[:, 61, 1]):.2f} (max {kbr[:, 61, 1].max():.2f})")
+        if os.environ.get("CL"):  # clock64 stamps (same SM): sync1, reduce, sync2 durations in clk
+            c = kb[:, 60:62, :].reshape(len(kb), 4).astype(np.int64)
+            d = np.diff(c, axis=1)
+            print(f"     cluster clk: sync1 p50 {np.median(d[:, 0]):.0f} max {d[:, 0].max():.0f} | reduce p50 "
+                  f"{np.median(d[:, 1]):.0f} max {d[:, 1].max():.0f} | sync2 p50 {np.median(d[:, 2]):.0f} max {d[:, 2].max():.0f}")
         if os.environ.get("KB"):
             kbr = np.where(kb > 0, kb.astype(np.int64) - t0, -1) / 1e3
             print("     kb issue-stamp:", " ".join(f"{v:.2f}" for v in kbr[0, :8, 0]), "| mma saw:",
