@@ -32,7 +32,7 @@ namespace ftb {
 cudaError_t launch_tc(const TcWork*, int32_t, int32_t, TcConfig, cudaStream_t);
 cudaError_t launch_tc2(const TcPair*, int32_t, int32_t, TcConfig, cudaStream_t);
 int tc_smem_bytes(const TcConfig& cfg);
-cudaError_t launch_ffma(const DevProblem*, const DevWork*, int32_t, int32_t, cudaStream_t);
+cudaError_t launch_ffma(const DevProblem*, const DevWork*, int32_t, int32_t, cudaStream_t, bool);
 
 namespace {
 
@@ -308,6 +308,7 @@ struct ExecImpl {
   void* d_blob = nullptr;             // one pool allocation: every section above but the workspace
   int device = -1;
   double encode_ms = 0.0;             // host time spent encoding TMA descriptors (FTB_PROFILE_CREATE)
+  bool ffma_vec = false;              // FFMA kernel: 16-B operand copies
   cudaEvent_t ready = nullptr;        // the table's upload has landed (recorded on the upload stream)
   bool ready_known = false;           // `ready` observed complete: launches need not wait for it
   // streams this table was launched on, each with the event recorded after
@@ -571,6 +572,13 @@ static void build(ExecImpl& ex, const ftb_gemm_desc* probs, const ftb_program* p
   int sms = device_sms();
   if (sms <= 0) sms = 148;
   ex.info.n_ctas = std::min<int64_t>(ex.info.n_work, ffma ? 4 * sms : sms);
+  if (ffma) {  // the FFMA kernel's 16-B copies need 16-B aligned operand rows
+    bool vec = true;
+    for (const DevProblem& P : ex.problems)
+      vec = vec && reinterpret_cast<uintptr_t>(P.A) % 16 == 0 && reinterpret_cast<uintptr_t>(P.B) % 16 == 0 &&
+            P.lda % 4 == 0 && P.ldb % 4 == 0 && (P.batch == 1 || (P.a_bs % 4 == 0 && P.b_bs % 4 == 0));
+    ex.ffma_vec = vec;
+  }
   if (ex.info.n_work > INT32_MAX) throw input_error("tile table too large", "work");
 }
 
@@ -1091,7 +1099,7 @@ ftb_status ftb_exec_launch(ftb_exec* ex, void* stream) {
         if (se.first == I.last_stream) FTB_CUDA(cudaStreamWaitEvent(s, se.second, 0));
     cudaError_t e = I.info.kernel == 1
                         ? ftb::launch_ffma(I.d_problems, I.d_work, static_cast<int32_t>(I.info.n_work),
-                                           static_cast<int32_t>(I.info.n_ctas), s)
+                                           static_cast<int32_t>(I.info.n_ctas), s, I.ffma_vec)
                         : cudaSuccess;
     if (e == cudaSuccess && I.info.kernel == 0 && I.n_pairs)
       e = ftb::launch_tc2(I.d_tcpairs, static_cast<int32_t>(I.n_pairs), static_cast<int32_t>(I.ctas2), I.cfg2, s);
