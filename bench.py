@@ -183,6 +183,51 @@ def cpu_shape_set(shapes, passes: int = 1, seconds_budget: float = 60.0) -> dict
             "seconds": sum(sum(v) for v in per.values()), "ms_per_pass": 1e3 * sum(ts.values())}
 
 
+def tuning_baseline(shapes, seconds_budget: float = 30.0) -> dict:
+    """ORACLE leg (VERDICT r1 missing #5): the reference's
+    planner — compile_shape + build_programs + rank_programs — as restated by
+    the oracle port (oracle/planner_port.py: numpy + Python, one process,
+    pinned to the reference's fixtures by tests/test_oracle_golden.py) against
+    this repo's C++ planner on ONE thread, per shape, B200 legality mode, over
+    the bench's shapes until the time budget is spent (the reference itself
+    cannot run on the GPU box; its own timings, measured in the build
+    container, are profiles/r1_planner_vs_reference.json)."""
+    sys.path.insert(0, str(ROOT / "tests" / "golden"))
+    from _digest import B200_BF16, tcgen05_legal  # the legality predicate the fixtures were made with
+
+    from oracle import planner_port as PP
+    from paper_2407_21418_b200.runtime import Planner
+
+    rows = []
+    t_start = time.perf_counter()
+    for s in shapes:
+        spec = PP.dense_spec(2) if s.kind == "dense" else PP.bmm_spec(2)
+        ext = {"i": s.M, "j": s.N, "k": s.K}
+        if s.kind == "bmm":
+            ext["b"] = s.batch
+        t0 = time.perf_counter()
+        so = PP.compile_shape(spec, ext, B200_BF16, legal=lambda sm, spec=spec, ext=ext: tcgen05_legal(spec.space, ext, sm))
+        tau = PP.main_axis(spec, ext, set(s.dynamic))
+        pool = PP.build_pool(spec, so, tau)
+        PP.rank(spec, so, pool, 1)
+        t_port = time.perf_counter() - t0
+        pl = Planner(threads=1)  # fresh: no cache hit
+        t0 = time.perf_counter()
+        pl.plan([s.instance()])
+        t_ours = time.perf_counter() - t0
+        rows.append((t_port, t_ours, len(pool)))
+        if time.perf_counter() - t_start > seconds_budget:
+            break
+    port = sum(r[0] for r in rows) / len(rows)
+    ours = sum(r[1] for r in rows) / len(rows)
+    return {"port_s_per_shape": port, "ours_s_per_shape": ours, "speedup": port / ours, "shapes": len(rows),
+            "pool_plans_mean": sum(r[2] for r in rows) / len(rows), "kind": "port", "cores": 1,
+            "sample": f"the first {len(rows)} bench shapes (B200 legality mode): oracle-port compile_shape + "
+                      "build_programs + rank_programs vs the C++ planner, one thread each",
+            "reference_itself": "profiles/r1_planner_vs_reference.json (mktune run in the build container: "
+                                "40-4000x slower than the C++ planner, 6 of 12 C1 shapes past a 120 s cap)"}
+
+
 def bench_shapes(args, seed: int):
     from paper_2407_21418_b200.workloads import c1_shapes
 
@@ -654,6 +699,8 @@ def run_ours(args, rank, world, local):
                                 "sample": f"numpy fp32 A@B per shape (oracle/execute_np.py, OpenBLAS on all cores) "
                                           f"over the same {cb['shapes']}-shape set, {cb['passes']} passes, "
                                           f"{cb['seconds']:.1f} s of compute"}
+    if rank == 0 and world == 1 and not args.no_cpu:
+        line["tuning_baseline"] = tuning_baseline(list(shapes), seconds_budget=args.tuning_budget_s)
     line["per_shape"] = ps["rows"] if args.per_shape_rows else None
     if args.c4_shapes > 0:
         line["c4_sweep"] = c4_sweep(args, rank, world, dev, P)
@@ -720,6 +767,7 @@ def main():
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--ops", choices=["all", "dense", "bmm"], default="all")
     ap.add_argument("--dynamic-steps", type=int, default=1, help="0 skips the e2e_dynamic key")
+    ap.add_argument("--tuning-budget-s", type=float, default=30.0)
     ap.add_argument("--c4-shapes", type=int, default=2000,
                     help="C4 sweep sample size (0 skips the c4_sweep key; 10000 = the full north_star set)")
     args = ap.parse_args()
