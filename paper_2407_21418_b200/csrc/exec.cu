@@ -311,6 +311,7 @@ struct ExecImpl {
   bool ffma_vec = false;              // FFMA kernel: 16-B operand copies
   cudaEvent_t ready = nullptr;        // the table's upload has landed (recorded on the upload stream)
   bool ready_known = false;           // `ready` observed complete: launches need not wait for it
+  bool captured = false;              // launched inside a stream capture: never freed (see ~ExecImpl)
   // streams this table was launched on, each with the event recorded after
   // its last launch: destroy frees only after all of them (stream order)
   std::vector<std::pair<cudaStream_t, cudaEvent_t>> launched;
@@ -341,7 +342,10 @@ struct ExecImpl {
       if (rs) cudaStreamWaitEvent(rs, se.second, 0);
       cudaEventDestroy(se.second);  // the wait above captured its state
     }
-    if (rs) {
+    // A table that was launched inside a stream capture may still be replayed
+    // by that CUDA graph after this handle is gone: its memory is deliberately
+    // kept (not freed) so no graph can ever read a recycled table.
+    if (rs && !captured) {
       if (d_blob) cudaFreeAsync(d_blob, rs);
       if (d_split_ws) cudaFreeAsync(d_split_ws, rs);
     }
@@ -1083,8 +1087,8 @@ ftb_status ftb_exec_launch(ftb_exec* ex, void* stream) {
     const bool capturing = cap != cudaStreamCaptureStatusNone;
     // Launches of one table are stream ordered (they share the split-K
     // workspace): a launch on a new stream first waits for the previous one.
-    // Captured launches are not tracked — a graph holding this table must not
-    // outlive it (as with any buffer the graph references).
+    // A captured launch marks the table as never-to-be-freed: the graph may
+    // replay it after the handle is destroyed.
     if (I.ready && !I.ready_known) {  // the table upload (create did not wait for it)
       if (capturing) {
         FTB_CUDA(cudaEventSynchronize(I.ready));  // a graph must not depend on an outside event
@@ -1106,6 +1110,7 @@ ftb_status ftb_exec_launch(ftb_exec* ex, void* stream) {
     if (e == cudaSuccess && I.info.kernel == 0 && I.n_singles)
       e = ftb::launch_tc(I.d_tcwork, static_cast<int32_t>(I.n_singles), static_cast<int32_t>(I.ctas1), I.cfg, s);
     if (e != cudaSuccess) throw ftb::cuda_error(std::string("kernel launch: ") + cudaGetErrorString(e));
+    if (capturing) I.captured = true;
     if (!capturing) {  // destroy frees the table only after this launch (exec.cu ~ExecImpl)
       cudaEvent_t ev = nullptr;
       for (auto& se : I.launched)

@@ -205,3 +205,31 @@ def test_sharded_c4_executor_single_rank(cuda, planner):
     _, merged2 = run_sharded(shapes, 0, 1, planner, 1.6792e15, execute=ex2)
     assert ex2.stats["chunks"] > ex.stats["chunks"]
     assert [r.checksum for r in merged2] == [r.checksum for r in merged]
+
+
+def test_captured_table_survives_destroy(cuda):
+    """A table launched inside a CUDA-graph capture stays valid for the
+    graph after its handle is destroyed (the runtime's table LRU may evict it
+    at any time): replays after close() still compute the right result."""
+    from paper_2407_21418_b200.execute import Executable, gemm_desc
+    from paper_2407_21418_b200.runtime import Planner, dense_instance
+
+    g = torch.Generator(device="cpu").manual_seed(2)
+    A = (torch.rand(300, 768, generator=g) * 2 - 1).bfloat16().to(cuda)
+    W = (torch.rand(768, 768, generator=g) * 2 - 1).bfloat16().to(cuda)
+    C = torch.empty(300, 768, dtype=torch.bfloat16, device=cuda)
+    ex = Executable([gemm_desc(A, W, C, "nk")], [Planner().plan([dense_instance(300, 768, 768)])[0].program])
+    s = torch.cuda.Stream(cuda)
+    ex.launch(s)
+    torch.cuda.synchronize()
+    graph = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(graph, stream=s):
+        ex.launch(s)
+    ex.close()
+    for _ in range(3):  # churn the pool with other tables
+        Executable([gemm_desc(A, W, C, "nk")], [Planner().plan([dense_instance(300, 768, 768)])[0].program]).close()
+    C.zero_()
+    torch.cuda.synchronize()
+    graph.replay()
+    torch.cuda.synchronize()
+    assert close(C, A.double() @ W.double().t(), 768, "replay after close")
