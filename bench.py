@@ -426,6 +426,79 @@ def e2e_per_shape(ss, planner, dev, passes: int):
             "ms_per_pass": 1e3 * sum(ts), "h2d": h2d, "d2h": d2h}
 
 
+def e2e_per_shape_pipelined(ss, planner, dev, iters: int = 16):
+    """The shape-set-mean metric end to end through the public API
+    (Planner.dense / Planner.bmm), per shape as a serving loop: every
+    iteration moves that shape's activations H2D from pinned host memory,
+    runs the GEMM and moves its whole output D2H to pinned host memory; two
+    device buffer sets alternate so iteration i+1's H2D and iteration i-1's
+    D2H (separate copy streams, full duplex) overlap iteration i's GEMM.
+    Per-shape time = (first H2D start -> last D2H end) / iters, fill and
+    drain included; weights stay resident."""
+    import torch
+
+    comp = torch.cuda.current_stream(dev)
+    h2d_s, d2h_s = torch.cuda.Stream(dev), torch.cuda.Stream(dev)
+    ts = []
+    h2d_bytes = d2h_bytes = 0
+    for x in ss.bound:
+        sh = x.shape
+        # set 0: the ShapeSet's own buffers; set 1: a twin with the same layout
+        dev_sets = [(x.inputs, x.A, x.B, x.C, x.C_store)]
+        twin_in = [t.clone() for t in x.inputs]
+        if sh.kind == "dense":
+            A1, B1 = twin_in[0], x.B
+        elif sh.name == "scores":
+            A1, B1 = twin_in[0], twin_in[1]
+        else:
+            A1, B1 = twin_in[0][:, :, : sh.K], twin_in[1]
+        C1s = torch.empty_like(x.C_store)
+        C1 = C1s.as_strided(x.C.size(), x.C.stride())
+        dev_sets.append((twin_in, A1, B1, C1, C1s))
+        host_in = [[t.cpu().pin_memory() for t in x.inputs] for _ in range(2)]
+        host_out = [x.C_store.cpu().pin_memory() for _ in range(2)]
+
+        def launch(k):
+            _, A, B, C, _ = dev_sets[k % 2]
+            if sh.kind == "dense":
+                planner.dense(A, B, b_layout=sh.b_layout, out=C, stream=comp)
+            else:
+                planner.bmm(A, B, b_layout=sh.b_layout, dynamic=sh.dynamic, out=C, stream=comp)
+
+        for k in range(2):  # warm both buffer sets' plan / table caches
+            launch(k)
+        torch.cuda.synchronize(dev)
+        comp_done = [torch.cuda.Event() for _ in range(iters)]
+        out_done = [torch.cuda.Event() for _ in range(iters)]
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(h2d_s)
+        for k in range(iters):
+            ins, _, _, _, Cs = dev_sets[k % 2]
+            if k >= 2:
+                h2d_s.wait_event(comp_done[k - 2])  # this set's previous inputs are consumed
+            with torch.cuda.stream(h2d_s):
+                for dst, src in zip(ins, host_in[k % 2]):
+                    dst.copy_(src, non_blocking=True)
+                in_done = torch.cuda.Event()
+                in_done.record(h2d_s)
+            comp.wait_event(in_done)
+            if k >= 2:
+                comp.wait_event(out_done[k - 2])  # ... and its previous output was read back
+            launch(k)
+            comp_done[k].record(comp)
+            d2h_s.wait_event(comp_done[k])
+            with torch.cuda.stream(d2h_s):
+                host_out[k % 2].copy_(Cs, non_blocking=True)
+                out_done[k].record(d2h_s)
+        e1.record(d2h_s)
+        torch.cuda.synchronize(dev)
+        ts.append(e0.elapsed_time(e1) * 1e-3 / iters)
+        h2d_bytes += sum(t.numel() * t.element_size() for t in x.inputs)
+        d2h_bytes += x.C_store.numel() * x.C_store.element_size()
+    return {"mean_tflops": sum(x.shape.flops / t for x, t in zip(ss.bound, ts)) / len(ts) / 1e12,
+            "ms_per_pass": 1e3 * sum(ts), "h2d": h2d_bytes, "d2h": d2h_bytes}
+
+
 def e2e_dynamic(planner, dev, steps: int, draws: int = 24, seed: int = 100):
     """Dynamic-shape serving loop, end to end (VERDICT r1 missing #4; the
     paper counts runtime plan construction inside inference time,
@@ -637,8 +710,9 @@ def run_ours(args, rank, world, local):
     }
 
     # ------------------------------------------------ end to end through the public API
-    e2e = e2e_per_shape(ss, planner, dev, passes=max(3, args.steps // 4))
+    e2e = e2e_per_shape_pipelined(ss, planner, dev)
     e2e_value = sum_over_ranks(e2e["mean_tflops"], world)
+    e2e_serial = e2e_per_shape(ss, planner, dev, passes=max(3, args.steps // 4))
     dyn = e2e_dynamic(planner, dev, steps=max(10, args.steps)) if args.dynamic_steps else None
 
     # ------------------------------------------------ roofline of the headline launches
@@ -683,8 +757,13 @@ def run_ours(args, rank, world, local):
         "grouped_step": grouped,
         "e2e": {"value": e2e_value, "unit": "TFLOP/s", "h2d_bytes_per_step": e2e["h2d"],
                 "d2h_bytes_per_step": e2e["d2h"], "ms_per_step": e2e["ms_per_pass"],
-                "mode": "shape-set mean through Planner.dense/bmm: per shape, activations H2D from pinned host "
-                        "memory + launch + output D2H to pinned memory inside its event window (weights resident)"},
+                "mode": "shape-set mean through Planner.dense/bmm, each shape as a serving loop of 16 iterations: "
+                        "every iteration H2D of its activations from pinned host memory + the GEMM + D2H of its whole "
+                        "output to pinned memory, copies of neighbouring iterations overlapped (two device buffer sets, "
+                        "separate H2D / D2H streams), fill and drain included; weights resident"},
+        "e2e_serial": {"value": sum_over_ranks(e2e_serial["mean_tflops"], world), "unit": "TFLOP/s",
+                       "ms_per_step": e2e_serial["ms_per_pass"],
+                       "mode": "latency view: per shape H2D + GEMM + D2H back to back on one stream, nothing overlapped"},
         "e2e_dynamic": dyn,
         "gpu_launches": ps["launches"] + args.steps,
         "gpu_launches_def": "per-shape timed launches (sum over shapes of steps x chain length) + grouped steps",
