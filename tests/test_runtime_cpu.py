@@ -107,3 +107,48 @@ def test_plan_cache_roundtrip(planned, tmp_path):
     again = pl2.plan(SHAPES)
     for a, b in zip(recs, again):
         assert a.describe()["parts"] == b.describe()["parts"]
+
+
+def test_gemm_desc_rejects_operands_that_disagree():
+    """the TMA descriptors and the work table are built from these
+    extents, so B's K / batch and C's shape must agree with A (checked before
+    anything touches a device; CPU tensors suffice)."""
+    import pytest
+    import torch
+
+    from paper_2407_21418_b200.execute import gemm_desc
+
+    bf = torch.bfloat16
+    A = torch.zeros(16, 64, dtype=bf)
+    with pytest.raises(ValueError, match="inner dimensions"):
+        gemm_desc(A, torch.zeros(32, 128, dtype=bf), torch.zeros(16, 128, dtype=bf), "kn")   # B has K = 32
+    with pytest.raises(ValueError, match="inner dimensions"):
+        gemm_desc(A, torch.zeros(128, 32, dtype=bf), torch.zeros(16, 128, dtype=bf), "nk")   # B^T has K = 32
+    with pytest.raises(ValueError, match="C has shape"):
+        gemm_desc(A, torch.zeros(64, 128, dtype=bf), torch.zeros(16, 100, dtype=bf), "kn")
+    with pytest.raises(ValueError, match="Dense needs"):
+        gemm_desc(A, torch.zeros(2, 64, 128, dtype=bf), torch.zeros(16, 128, dtype=bf), "kn")
+    A3 = torch.zeros(4, 16, 64, dtype=bf)
+    with pytest.raises(ValueError, match="B has batch"):
+        gemm_desc(A3, torch.zeros(3, 64, 32, dtype=bf), torch.zeros(4, 16, 32, dtype=bf), "kn")
+    with pytest.raises(ValueError, match="C has shape"):
+        gemm_desc(A3, torch.zeros(4, 64, 32, dtype=bf), torch.zeros(4, 16, 31, dtype=bf), "kn")
+    with pytest.raises(ValueError, match="b_layout"):
+        gemm_desc(A, torch.zeros(64, 128, dtype=bf), torch.zeros(16, 128, dtype=bf), "xx")
+    with pytest.raises(ValueError, match="CUDA tensor"):  # consistent shapes reach the device check
+        gemm_desc(A, torch.zeros(64, 128, dtype=bf), torch.zeros(16, 128, dtype=bf), "kn")
+
+
+def test_plan_cache_key_covers_the_whole_descriptor():
+    """Two descriptors with the same name but different tcgen05 fields must
+    not share plan-cache entries (runtime.Planner keys on the full doc)."""
+    import dataclasses
+
+    from paper_2407_21418_b200.mktune.hardware import b200_bf16
+    from paper_2407_21418_b200.runtime import Planner, dense_instance
+
+    base = b200_bf16(tcgen05=True)
+    a, b = Planner(hw=base), Planner(hw=dataclasses.replace(base, mma_n_max=128, tmem_columns=256))
+    inst = dense_instance(1216, 2304, 768)
+    assert a._key(inst) != b._key(inst)
+    assert a._key(inst) == Planner(hw=base)._key(inst)
