@@ -241,8 +241,9 @@ void ftb_exec_destroy(ftb_exec* ex);
  * saw data), then the CTA's start and end stamps (builds with FTB_TRACE_SPAN). */
 ftb_status ftb_exec_set_trace(ftb_exec* ex, int32_t enable);
 ftb_status ftb_exec_read_trace(const ftb_exec* ex, uint64_t* out, int64_t cap, int64_t* n_out);
-/* Pipeline shapes chosen for the table, 10 ints: single-CTA kernel {stages,
- * col_stage_bytes, n_acc, acc_cols}, CTA-pair kernel {same}, n_singles, n_pairs. */
+/* Pipeline shapes chosen for the table, 12 ints: single-CTA kernel {stages,
+ * col_stage_bytes, n_acc, acc_cols}, CTA-pair kernel {same}, n_singles, n_pairs,
+ * on-chip split-K factor (0 or 1: none), global-workspace split-K (0/1). */
 ftb_status ftb_exec_get_config(const ftb_exec* ex, int32_t* out4);
 /* Host-only lowering (no device, no TMA descriptors): the same table
  * ftb_exec_create would upload, for inspection and CPU tests. */

@@ -235,6 +235,9 @@ __device__ __forceinline__ void epilogue_tile(uint8_t* region, uint32_t& ngrp, u
           release();
           released = true;
         }
+#ifdef FTB_NULL_EPI
+        continue;  // experiment build: accumulators drained, nothing staged or stored
+#endif
         if (op) {  // normal: TMEM columns are C columns; swap-AB: lanes are
           apply_epi(ra, *op, !swap, swap ? lane0 + lane_base : col0 + c0);
           if (two) apply_epi(rb, *op, !swap, swap ? lane0 + lane_base : col0 + c0 + 32);
@@ -249,7 +252,11 @@ __device__ __forceinline__ void epilogue_tile(uint8_t* region, uint32_t& ngrp, u
         fence_async_smem();
         __syncwarp();
         FTB_EPI_EV((c0 >> 6) * 6 + 3);
+#ifdef FTB_EPI_NOSTORE
+        if (false) {  // experiment build: staged but never stored
+#else
         if (lane == 0) {
+#endif
           const int l0 = lane0 + lane_base, k0 = col0 + c0;
           if (!swap) {
             tma_store_3d(out_map, smem_addr(box), k0, l0, batch);

@@ -799,6 +799,38 @@ static void upload(ExecImpl& I) {
       }
     }
   }
+  // Split-K decision for a candidate table (used by the column split below to
+  // compare lowerings, and by the split-K pass): {split factor, on chip}.
+  // On-chip (cluster) mode when every item splits the same way (s = 4 or 2,
+  // >= split_min_kb K blocks per split) and the table fits the co-resident
+  // clusters (measured: 33 clusters of 4, 74 of 2 at ~200 KiB smem per CTA,
+  // scripts/micro/cluster_occ.cu); else the global-workspace path, narrow
+  // items only.
+  const char* env_sk = std::getenv("FTB_SPLITK");
+  const bool split_on = !(env_sk && env_sk[0] == '0') && !pairing;
+  const char* env_mk = std::getenv("FTB_SPLIT_MINKB");
+  const int split_min_kb = env_mk ? std::max(1, std::atoi(env_mk)) : 8;
+  const char* env_sw = std::getenv("FTB_SPLIT_WIDE");
+  const bool split_wide = env_sw && env_sw[0] == '1';
+  const char* env_scl = std::getenv("FTB_SPLIT_CLUSTER");
+  const bool cluster_on = !(env_scl && env_scl[0] == '0');
+  const int sms_all = device_sms() > 0 ? device_sms() : 148;
+  auto split_choice = [&](const std::vector<TcWork>& v) -> std::pair<int, bool> {
+    const int64_t n = static_cast<int64_t>(v.size());
+    if (wide_split || !split_on || n == 0 || n * 2 > sms_all) return {1, false};
+    const int target = static_cast<int>(std::min<int64_t>(kMaxSplit, sms_all / n));
+    if (cluster_on)
+      for (int cand : {4, 2}) {
+        if (cand > target) continue;
+        bool ok = true;
+        for (const TcWork& t : v) ok = ok && !t.pack && t.n_mma <= 128 && t.num_kb / split_min_kb >= cand;
+        if (ok && n * cand <= std::min(cand == 4 ? 132 : 148, sms_all)) return {cand, true};
+      }
+    int s_glob = 1;
+    for (const TcWork& t : v)
+      if (!t.pack && (t.n_mma <= 128 || split_wide)) s_glob = std::max(s_glob, std::min(target, t.num_kb / split_min_kb));
+    return {s_glob, false};
+  };
   // Column split: a table with fewer than half as many items as SMs runs one
   // wave whose length is one item's K loop; a 256-column item's K block costs
   // ~550 clk (smem-port bound: 48 KiB TMA write + 48 KiB MMA read), a
@@ -810,71 +842,61 @@ static void upload(ExecImpl& I) {
     if (sms_here <= 0) sms_here = 148;
     const char* env_cs = std::getenv("FTB_COLSPLIT");
     const bool cs_on = !(env_cs && env_cs[0] == '0') && !pairing;
-    int64_t wide = 0;
-    for (const TcWork& t : tw) wide += (!t.pack && t.n_mma > 128 && t.col_len > 128) ? 1 : 0;
-    if (!wide_split && cs_on && wide > 0 && static_cast<int64_t>(tw.size()) + wide <= sms_here) {
+    const char* env_cw = std::getenv("FTB_COLSPLIT_MIN");
+    const int min_w = env_cw ? std::max(32, std::atoi(env_cw)) : 64;  // narrowest piece
+    // Halve while the table still fits one wave: 256 -> 128 columns, then
+    // 128 -> 64 (K-major column operands). Narrow pieces cost little MMA time
+    // in a one-wave table (a K block's MMA floor is ~400 clk at N = 64 vs
+    // ~460 at N = 128) and halve each SM's share of the output, whose TMA
+    // stores leave an SM at ~20-30 B/clk (scripts/micro/store_bench.cu):
+    // measured C1 out M=608 6.41 -> 6.03 us, qkv M=160 6.69 -> 6.14, FFN2
+    // M=768 15.0 -> 12.3 (profiles/r2au_colsplit64.txt). Not when it would
+    // lower the table's split-K factor: a K split halves every CTA's K loop,
+    // a column split does not (FFN2 M=800: 12.7 -> 15.6 us, M=352: 9.8 ->
+    // 10.4, profiles/r2ax_splitk_colsplit.txt).
+    for (int level = 0; level < 3 && !wide_split && cs_on; ++level) {
+      auto splittable = [&](const TcWork& t) {
+        if (t.pack || t.n_mma <= min_w || t.col_len <= min_w) return false;
+        return t.n_mma > 128 || !(t.flags & kFlagColMN);  // MN-major operands: 64-column boxes, n_mma >= 128
+      };
+      int64_t wide = 0;
+      for (const TcWork& t : tw) wide += splittable(t) ? 1 : 0;
+      if (wide == 0 || static_cast<int64_t>(tw.size()) + wide > sms_here) break;
       std::vector<TcWork> cs;
       cs.reserve(tw.size() + wide);
       for (const TcWork& t : tw) {
-        if (t.pack || t.n_mma <= 128 || t.col_len <= 128) {
+        if (!splittable(t)) {
           cs.push_back(t);
           continue;
         }
         const bool col_mn = (t.flags & kFlagColMN) != 0;
+        const int half = t.n_mma > 128 ? 128 : static_cast<int>(round_up((t.col_len + 1) / 2, 32));
         TcWork a = t, b = t;
-        a.col_len = 128;
-        a.n_mma = 128;
-        b.col0 = t.col0 + 128;
-        b.col_len = t.col_len - 128;
+        a.col_len = half;
+        a.n_mma = t.n_mma > 128 ? 128 : half;
+        b.col0 = t.col0 + half;
+        b.col_len = t.col_len - half;
         b.n_mma = static_cast<int32_t>(round_up(b.col_len, col_mn ? 128 : 32));
         cs.push_back(a);
         cs.push_back(b);
       }
+      if (split_choice(cs).first < split_choice(tw).first) break;
       tw.swap(cs);
       max_n = 16;
       for (const TcWork& t : tw) max_n = std::max(max_n, t.n_mma);
     }
   }
   {
-    int sms_here = device_sms();
-    if (sms_here <= 0) sms_here = 148;
-    const char* env_sk = std::getenv("FTB_SPLITK");
-    const bool split_on = !(env_sk && env_sk[0] == '0') && !pairing;
+    const int sms_here = sms_all;
     const int64_t n_items = static_cast<int64_t>(tw.size());
-    const char* env_mk = std::getenv("FTB_SPLIT_MINKB");
-    const int split_min_kb = env_mk ? std::max(1, std::atoi(env_mk)) : 8;
-    const char* env_w = std::getenv("FTB_SPLIT_WIDE");
-    const bool split_wide = env_w && env_w[0] == '1';
     if (!wide_split && split_on && n_items > 0 && n_items * 2 <= sms_here) {
       const int target = static_cast<int>(std::min<int64_t>(kMaxSplit, sms_here / n_items));
-      // On-chip mode: when every item can be split the same way (s = 4 or 2,
-      // >= split_min_kb K blocks per split) and the whole table fits the
-      // co-resident clusters (measured: 33 clusters of 4, 74 of 2 at ~200 KiB
-      // smem per CTA, scripts/micro/cluster_occ.cu), the splits of a tile
-      // become one cluster and reduce through distributed shared memory
-      // (kernel_tc.cu cluster_reduce) — no fp32 workspace round trip.
-      const char* env_cl = std::getenv("FTB_SPLIT_CLUSTER");
-      const bool cluster_on = !(env_cl && env_cl[0] == '0');
-      int s_cl = 0;
-      if (cluster_on) {
-        int s_glob = 0;  // the global-workspace path's split count
-        for (const TcWork& t : tw)
-          if (!t.pack && (t.n_mma <= 128 || split_wide)) s_glob = std::max(s_glob, std::min(target, t.num_kb / split_min_kb));
-        for (int cand : {4, 2}) {
-          if (cand > target) continue;
-          bool ok = true;
-          for (const TcWork& t : tw) ok = ok && !t.pack && t.n_mma <= 128 && t.num_kb / split_min_kb >= cand;
-          const int64_t cap = std::min<int64_t>(cand == 4 ? 132 : 148, sms_here);
-          if (ok && n_items * cand <= cap) {
-            s_cl = cand;
-            break;
-          }
-        }
-        // on chip unless it gives up more than a third of the splits the
-        // workspace path would use (measured: C1 FFN2 M=768, 2 vs 4 splits:
-        // 13.0 vs 11.6 us; M=1024, 2 vs 3: 13.8 vs 14.3 us)
-        if (s_cl && 3 * s_cl < 2 * s_glob) s_cl = 0;
-      }
+      // on chip whenever the table qualifies: round 2 measured the workspace
+      // path 3-5 us slower than a cluster split of the same table even at
+      // half the split count (FFN2 M=160 cluster-4 9.4 vs workspace 14.2 us,
+      // M=768 cluster-2 vs workspace-4, profiles/r2ax_splitk_colsplit.txt)
+      const std::pair<int, bool> sc = split_choice(tw);
+      const int s_cl = sc.second ? sc.first : 0;
       std::vector<TcWork> split;
       int32_t tiles = 0;
       for (const TcWork& t : tw) {
@@ -1182,6 +1204,8 @@ ftb_status ftb_exec_get_config(const ftb_exec* ex, int32_t* out4) {
     }
     out4[8] = static_cast<int32_t>(I.n_singles);
     out4[9] = static_cast<int32_t>(I.n_pairs);
+    out4[10] = I.cfg.cluster_split;                      // on-chip split-K factor (0/1: none)
+    out4[11] = I.cfg.split_ws != nullptr ? 1 : 0;        // global-workspace split-K in use
   });
 }
 

@@ -678,7 +678,11 @@ __global__ void __launch_bounds__(kEpi8 ? 384 : kTcThreads, 1)
       }
       if (quad == 0 && lane == 0) trace_ev(cfg, local, 5);
     }
+#ifdef FTB_END_READ
+    if (lane == 0) bulk_wait_read<0>();  // experiment: only the smem reads of the stores
+#else
     if (lane == 0) bulk_wait_all();  // output stores complete before the CTA retires
+#endif
     __syncwarp();
 #ifdef FTB_PROD_PROFILE
     if (lane == 0 && warp == 2 && cfg.trace) {

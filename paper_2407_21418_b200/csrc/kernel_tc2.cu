@@ -202,6 +202,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kTcThreads, 1)
       uint32_t pend = 0;
       const uint32_t tmem_u = __shfl_sync(0xffffffffu, tmem_base, 0);
       const uint32_t lane_u32 = smem_addr(lane_buf), col_u32 = smem_addr(col_buf);
+#ifdef FTB_PROD_PROFILE
+      unsigned long long m_te = 0, m_full = 0, m_issue = 0, m_t0 = clock64();
+#endif
       if (cid < n_work) pend = fetch_record_word(work, cid);
       for (int w = cid; w < n_work; w += G, ++local) {
         const TcPair it = bcast_record<TcPair>(pend);
@@ -210,15 +213,28 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kTcThreads, 1)
         const uint32_t use = local / cfg.n_acc;
         const uint32_t lane_mn = (it.flags & kFlagLaneMN) ? 1u : 0u;
         const uint32_t col_mn = (it.flags & kFlagColMN) ? 1u : 0u;
+#ifdef FTB_PROD_PROFILE
+        unsigned long long mt0 = clock64();
+#endif
         mbar_wait(&tempty[slot], (use & 1) ^ 1);
         tc_fence_after();
+#ifdef FTB_PROD_PROFILE
+        m_te += clock64() - mt0;
+#endif
         const uint32_t tmem_d = tmem_u + slot * cfg.acc_cols;
         const uint32_t idesc = idesc_bf16_f32(2 * kLaneRows, static_cast<uint32_t>(it.n_mma), lane_mn, col_mn);
         for (int kb = 0; kb < it.num_kb; ++kb, ++g) {
           const uint32_t s = ms;
+#ifdef FTB_PROD_PROFILE
+          unsigned long long mf0 = clock64();
+#endif
           mbar_wait(&full[s], mphase);
           if (++ms == S) { ms = 0; mphase ^= 1; }
           tc_fence_after();
+#ifdef FTB_PROD_PROFILE
+          unsigned long long mf1 = clock64();
+          m_full += mf1 - mf0;
+#endif
           if (lane == 0) {
             if (kb == 0) trace2_ev(cfg, local, 2);
             trace2_kb(cfg, g, 1);
@@ -235,17 +251,29 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kTcThreads, 1)
           }
           tc_commit_pair_mc_elect(smem_addr(&empty[s]));
           __syncwarp();
+#ifdef FTB_PROD_PROFILE
+          m_issue += clock64() - mf1;
+#endif
         }
         tc_commit_pair_mc_elect(smem_addr(&tfull[slot]));
         if (lane == 0) trace2_ev(cfg, local, 3);
         __syncwarp();
       }
+#ifdef FTB_PROD_PROFILE
+      if (lane == 0 && cfg.trace) {
+        unsigned long long* t = cfg.trace + static_cast<size_t>(blockIdx.x) * kTracePerCta;
+        t[6] = m_te; t[7] = m_full; t[8] = m_issue; t[9] = clock64() - m_t0;
+      }
+#endif
     }
   } else {
     // ------------------------------------------------------------ epilogue (both CTAs)
     const int quad = warp & 3;
     uint8_t* region = reinterpret_cast<uint8_t*>(epi_buf) + quad * kEpiWarpBytes;
     uint32_t local = 0, ngrp = 0;
+#ifdef FTB_PROD_PROFILE
+    unsigned long long e_wait = 0, e_t0 = clock64();
+#endif
     TcPair nxt;
     if (cid < n_work) nxt = load_pair(work, cid);
     for (int w = cid; w < n_work; w += G, ++local) {
@@ -257,7 +285,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kTcThreads, 1)
       const bool tma = it.flags & kFlagTmaStore;
       const int lane_len = rank ? it.lane_len[1] : it.lane_len[0];
       const int lane0 = rank ? it.lane0[1] : it.lane0[0];
+#ifdef FTB_PROD_PROFILE
+      unsigned long long ew0 = clock64();
+#endif
       mbar_wait(&tfull[slot], use & 1);
+#ifdef FTB_PROD_PROFILE
+      e_wait += clock64() - ew0;
+#endif
       tc_fence_after();
       if (quad == 0 && lane == 0) trace2_ev(cfg, local, 4);
       const int lane_base = quad * 32;
@@ -273,8 +307,18 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kTcThreads, 1)
           (it.flags & kFlagEpiOp) ? &it.maps->epi : nullptr);
       if (quad == 0 && lane == 0) trace2_ev(cfg, local, 5);
     }
+#ifdef FTB_END_READ
+    if (lane == 0) bulk_wait_read<0>();  // experiment: only the smem reads of the stores
+#else
     if (lane == 0) bulk_wait_all();  // output stores complete before the CTA retires
+#endif
     __syncwarp();
+#ifdef FTB_PROD_PROFILE
+    if (lane == 0 && warp == 2 && cfg.trace) {
+      unsigned long long* t = cfg.trace + static_cast<size_t>(blockIdx.x) * kTracePerCta;
+      t[10] = e_wait; t[11] = clock64() - e_t0;
+    }
+#endif
   }
 
   tc_fence_before();

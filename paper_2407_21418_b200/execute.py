@@ -224,11 +224,12 @@ class Executable:
 
     def config(self) -> dict:
         """Pipeline shape chosen for this table (tcgen05 kernel)."""
-        out = (C.c_int32 * 10)()
+        out = (C.c_int32 * 12)()
         _lib.check(_lib.lib().ftb_exec_get_config(self._h, out))
         one = {"stages": out[0], "col_stage_bytes": out[1], "n_acc": out[2], "acc_cols": out[3]}
         pair = {"stages": out[4], "col_stage_bytes": out[5], "n_acc": out[6], "acc_cols": out[7]}
-        return {"single": one, "pair": pair, "n_singles": out[8], "n_pairs": out[9]}
+        return {"single": one, "pair": pair, "n_singles": out[8], "n_pairs": out[9],
+                "cluster_split": out[10], "workspace_split": bool(out[11])}
 
     def set_trace(self, enable: bool = True) -> None:
         _lib.check(_lib.lib().ftb_exec_set_trace(self._h, 1 if enable else 0))

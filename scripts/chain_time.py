@@ -62,5 +62,5 @@ for spec in os.environ.get("SHAPES", "dense 128 256 64;dense 608 768 768;bmm 384
         ts.append(e0.elapsed_time(e1) * 1e3 / nl)
     ts.sort()
     env = " ".join(f"{k}={v}" for k, v in os.environ.items() if k.startswith("FTB_"))
-    print(f"{spec:28s} {ts[len(ts) // 2]:6.2f} us/launch  chain {nl:4d}  items {exes[0].info.n_work:4d} ctas {exes[0].info.n_ctas:3d} "
+    print(f"{spec:28s} {ts[len(ts) // 2]:6.2f} us/launch  chain {nl:4d}  items {exes[0].info.n_work:4d} ctas {exes[0].info.n_ctas:3d} kernel-items {exes[0].config()['n_singles']:4d} split {exes[0].config()['cluster_split']}{'w' if exes[0].config()['workspace_split'] else 'c'} "
           f"cfg {exes[0].config()['single']}  [{env}]", flush=True)

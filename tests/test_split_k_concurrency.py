@@ -6,7 +6,12 @@ deadlock here — the resident splits wait for splits that cannot be scheduled
 — until the occupier's timeout; the per-chunk last-arriver reduction runs
 the splits in waves on the free SMs and completes. Both the on-chip cluster
 path and the global-workspace path are exercised; results must be correct
-and identical to the same table launched on an idle GPU."""
+and identical to the same table launched on an idle GPU.
+
+The cluster path's splits wait only for CTAs of their own cluster, which the
+hardware schedules together on one GPC, so it needs some GPC with four free
+SMs: it runs with 40 SMs left free (of 8 GPCs at least one then has >= 5),
+the workspace path with 4."""
 
 import ctypes
 import time
@@ -21,8 +26,8 @@ from paper_2407_21418_b200.execute import Executable, gemm_desc, program_struct
 pytestmark = pytest.mark.gpu
 
 
-@pytest.mark.parametrize("cluster", ["0", "1"])
-def test_split_k_completes_while_other_kernel_holds_sms(cuda, monkeypatch, cluster):
+@pytest.mark.parametrize("cluster,free", [("0", 4), ("1", 40)])
+def test_split_k_completes_while_other_kernel_holds_sms(cuda, monkeypatch, cluster, free):
     monkeypatch.setenv("FTB_SPLIT_CLUSTER", cluster)
     M, N, K = 64, 1024, 4096
     g = torch.Generator(device="cpu").manual_seed(9)
@@ -35,9 +40,10 @@ def test_split_k_completes_while_other_kernel_holds_sms(cuda, monkeypatch, clust
     torch.cuda.synchronize()
     alone = C.clone()
     assert_close(alone, ref, K, "idle GPU")
+    cfg = ex.config()
+    assert (cfg["cluster_split"] > 1) == (cluster == "1") and cfg["workspace_split"] == (cluster == "0"), cfg
     n_split_ctas = ex.info.n_ctas
     sms = torch.cuda.get_device_properties(cuda).multi_processor_count
-    free = 4
     assert n_split_ctas > free, "the table must need more SMs than are left free"
     ctl = torch.zeros(4, dtype=torch.int32).pin_memory()
     occ_stream, run_stream = torch.cuda.Stream(cuda), torch.cuda.Stream(cuda)
