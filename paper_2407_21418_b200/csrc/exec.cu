@@ -843,9 +843,9 @@ static void upload(ExecImpl& I) {
     const char* env_cs = std::getenv("FTB_COLSPLIT");
     const bool cs_on = !(env_cs && env_cs[0] == '0') && !pairing;
     const char* env_cw = std::getenv("FTB_COLSPLIT_MIN");
-    const int min_w = env_cw ? std::max(32, std::atoi(env_cw)) : 64;  // narrowest piece
+    const int min_w = env_cw ? std::max(32, std::atoi(env_cw)) : 32;  // narrowest piece
     // Halve while the table still fits one wave: 256 -> 128 columns, then
-    // 128 -> 64 (K-major column operands). Narrow pieces cost little MMA time
+    // 128 -> 64 -> 32 (K-major column operands). Narrow pieces cost little MMA time
     // in a one-wave table (a K block's MMA floor is ~400 clk at N = 64 vs
     // ~460 at N = 128) and halve each SM's share of the output, whose TMA
     // stores leave an SM at ~20-30 B/clk (scripts/micro/store_bench.cu):
@@ -860,8 +860,17 @@ static void upload(ExecImpl& I) {
         return t.n_mma > 128 || !(t.flags & kFlagColMN);  // MN-major operands: 64-column boxes, n_mma >= 128
       };
       int64_t wide = 0;
-      for (const TcWork& t : tw) wide += splittable(t) ? 1 : 0;
-      if (wide == 0 || static_cast<int64_t>(tw.size()) + wide > sms_here) break;
+      bool to32 = false;
+      for (const TcWork& t : tw)
+        if (splittable(t)) {
+          ++wide;
+          to32 = to32 || t.n_mma <= 64;
+        }
+      // 32-column pieces only while the table stays within half the SMs
+      // (measured: out M=352 5.95 -> 5.76 us at 72 CTAs, M=608 6.02 -> 6.23
+      // at 120; profiles/r2az_colsplit32.txt)
+      const int64_t cap = to32 ? sms_here / 2 : sms_here;
+      if (wide == 0 || static_cast<int64_t>(tw.size()) + wide > cap) break;
       std::vector<TcWork> cs;
       cs.reserve(tw.size() + wide);
       for (const TcWork& t : tw) {
@@ -880,7 +889,9 @@ static void upload(ExecImpl& I) {
         cs.push_back(a);
         cs.push_back(b);
       }
-      if (split_choice(cs).first < split_choice(tw).first) break;
+      const int s_new = split_choice(cs).first;
+      if (s_new < split_choice(tw).first) break;
+      if (to32 && static_cast<int64_t>(cs.size()) * s_new > cap) break;  // CTAs after split-K (FFN2 M=160: 8.9 -> 9.3 us at 120)
       tw.swap(cs);
       max_n = 16;
       for (const TcWork& t : tw) max_n = std::max(max_n, t.n_mma);
