@@ -133,6 +133,12 @@ __device__ __forceinline__ void tma_store_3d(const CUtensorMap* m, uint32_t src,
                "r"(src), "r"(c0), "r"(c1), "r"(c2)
                : "memory");
 }
+// 1-D bulk copy shared -> global (16-B aligned addresses, size a multiple of 16)
+__device__ __forceinline__ void bulk_store_1d(void* gdst, uint32_t src, uint32_t bytes) {
+  asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(reinterpret_cast<uint64_t>(gdst)),
+               "r"(src), "r"(bytes)
+               : "memory");
+}
 __device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
 template <int N>
 __device__ __forceinline__ void bulk_wait_read() {
@@ -213,13 +219,94 @@ __device__ unsigned long long* ftb_epi_dbg;
   } while (0)
 #endif
 
+// kFlagBulkStore: this warp's C rows [lane0 + lane_base, + nrows) are whole
+// rows of a compact C (col_len == ldc), i.e. one contiguous byte range. Rows
+// are staged in the warp's 8 KiB region in C's own layout, at the same
+// address phase mod 16 as their destination, so one 1-D bulk copy writes the
+// 16-B aligned interior; the < 16 B head and tail go out as element stores.
+// (Scores BMMs with T % 8 != 0: their rows are not a multiple of 16 B, which
+// no TMA tensor map can describe.)
+template <class Release>
+__device__ __forceinline__ bool bulk_rows(uint8_t* region, uint32_t taddr, bool f32, void* C, int64_t ldc, int row0,
+                                          int nrows, int col_len, int col0, Release& release, const EpiOp* op) {
+  const int lane = threadIdx.x & 31;
+  const int esz = f32 ? 4 : 2;
+  const int rowb = col_len * esz;
+  const int rows_per = min(nrows, (8192 - 16) / rowb);
+  if (rows_per <= 0) return false;
+  char* gbase = static_cast<char*>(C) + static_cast<int64_t>(row0) * ldc * esz;
+  bool released = false;
+  for (int ra = 0; ra < nrows; ra += rows_per) {
+    const int rb = min(nrows, ra + rows_per);
+    char* g0 = gbase + static_cast<int64_t>(ra) * rowb;
+    const int nbytes = (rb - ra) * rowb;
+    const uintptr_t ga = reinterpret_cast<uintptr_t>(g0);
+    uint8_t* sb = region + (ga & 15u);
+    if (lane == 0) bulk_wait_read<0>();  // the region's previous bulk / TMA stores have read it
+    __syncwarp();
+    for (int c0 = 0; c0 < col_len; c0 += 32) {
+      uint32_t raw[32];
+      tmem_ld_32x32b_x32(taddr + c0, raw);
+      tmem_ld_wait();
+      if (rb >= nrows && c0 + 32 >= col_len) {  // last TMEM read of the item
+        release();
+        released = true;
+      }
+      if (op) apply_epi(raw, *op, true, col0 + c0);
+      if (lane >= ra && lane < rb) {
+        uint8_t* dst = sb + (lane - ra) * rowb + c0 * esz;
+        const int n = min(32, col_len - c0);
+        if (f32) {
+#pragma unroll
+          for (int e = 0; e < 32; ++e)
+            if (e < n) reinterpret_cast<float*>(dst)[e] = __uint_as_float(raw[e]);
+        } else {
+#pragma unroll
+          for (int e = 0; e < 32; ++e)
+            if (e < n) reinterpret_cast<__nv_bfloat16*>(dst)[e] = __float2bfloat16_rn(__uint_as_float(raw[e]));
+        }
+      }
+    }
+    fence_async_smem();
+    __syncwarp();
+    const uintptr_t a0 = (ga + 15) & ~uintptr_t(15), a1 = (ga + nbytes) & ~uintptr_t(15);
+    if (a1 > a0) {
+      if (lane == 0) {
+        bulk_store_1d(reinterpret_cast<void*>(a0), smem_addr(sb + (a0 - ga)), static_cast<uint32_t>(a1 - a0));
+        bulk_commit();
+      }
+      const int nh = static_cast<int>(a0 - ga) / esz, nt = static_cast<int>(ga + nbytes - a1) / esz;
+      int off = -1;
+      if (lane < nh) off = lane * esz;
+      else if (lane >= 16 && lane - 16 < nt) off = static_cast<int>(a1 - ga) + (lane - 16) * esz;
+      if (off >= 0) {
+        if (f32) __stcg(reinterpret_cast<float*>(g0 + off), *reinterpret_cast<const float*>(sb + off));
+        else __stcg(reinterpret_cast<unsigned short*>(g0 + off), *reinterpret_cast<const unsigned short*>(sb + off));
+      }
+    } else {
+      for (int off = lane * esz; off < nbytes; off += 32 * esz) {
+        if (f32) __stcg(reinterpret_cast<float*>(g0 + off), *reinterpret_cast<const float*>(sb + off));
+        else __stcg(reinterpret_cast<unsigned short*>(g0 + off), *reinterpret_cast<const unsigned short*>(sb + off));
+      }
+    }
+  }
+  if (!released) release();
+  return true;
+}
+
 template <class Release>
 __device__ __forceinline__ void epilogue_tile(uint8_t* region, uint32_t& ngrp, uint32_t taddr, bool active, bool tma,
                                               bool swap, bool f32, const CUtensorMap* out_map, void* C, int64_t ldc,
                                               int lane0, int lane_len, int lane_base, int col0, int col_len, int batch,
-                                              Release release, const EpiOp* op = nullptr) {
+                                              Release release, const EpiOp* op = nullptr, bool bulk = false,
+                                              int tail0 = 1 << 30) {
   const int lane = threadIdx.x & 31;
   bool released = false;
+  if (active && bulk && !tma && !swap &&
+      bulk_rows(region, taddr, f32, C, ldc, lane0 + lane_base, min(32, lane_len - lane_base), col_len, col0, release, op)) {
+    ngrp |= 0x80000000u;  // the last bulk copy may still read any part of the region (see below)
+    return;
+  }
   if (active) {
     if (tma) {
       // groups of two 32-column chunks: both tcgen05.ld in flight, one proxy
@@ -243,7 +330,12 @@ __device__ __forceinline__ void epilogue_tile(uint8_t* region, uint32_t& ngrp, u
           if (two) apply_epi(rb, *op, !swap, swap ? lane0 + lane_base : col0 + c0 + 32);
         }
         uint8_t* box = region + (ngrp & 1) * 4096;
-        if (lane == 0) bulk_wait_read<1>();  // the group that last used these boxes has read them
+        if (ngrp >> 31) {  // a bulk copy of a previous item spans both boxes
+          if (lane == 0) bulk_wait_read<0>();
+          ngrp &= 0x7fffffffu;
+        } else if (lane == 0) {
+          bulk_wait_read<1>();  // the group that last used these boxes has read them
+        }
         __syncwarp();
         FTB_EPI_EV((c0 >> 6) * 6 + 1);
         stage_box_bf16(box, ra, !swap);
@@ -252,6 +344,33 @@ __device__ __forceinline__ void epilogue_tile(uint8_t* region, uint32_t& ngrp, u
         fence_async_smem();
         __syncwarp();
         FTB_EPI_EV((c0 >> 6) * 6 + 3);
+        if (c0 + 64 > tail0 && lane < lane_len - lane_base) {
+          // kFlagTmaTail: columns [tail0, col_len) (< 8, starting on a
+          // multiple of 8, so inside one 16-B chunk of a staged box and at a
+          // 16-B aligned address of C) lie past the store map's end (N
+          // rounded down to 8); this lane's row writes them as 8 + 4 + 2 B
+          // pieces of that chunk (row `lane` of a box: chunk q at (q ^ ((lane >> 1) & 3)) * 16)
+          const int cc = (tail0 - c0) & 31;
+          const uint4 v = *reinterpret_cast<const uint4*>(box + ((tail0 - c0) >> 5) * 2048 + lane * 64 +
+                                                          (((cc >> 3) ^ ((lane >> 1) & 3)) * 16));
+          char* dst = reinterpret_cast<char*>(static_cast<__nv_bfloat16*>(C) +
+                                              static_cast<int64_t>(lane0 + lane_base + lane) * ldc + col0 + tail0);
+          const int n = col_len - tail0;
+          uint32_t w[4] = {v.x, v.y, v.z, v.w};
+          int at = 0;
+          if (n >= 4) {
+            *reinterpret_cast<uint2*>(dst) = make_uint2(w[0], w[1]);
+            at = 2;
+          }
+          if (n & 2) {
+            *reinterpret_cast<uint32_t*>(dst + at * 4) = at ? w[2] : w[0];
+            ++at;
+          }
+          if (n & 1) {
+            const uint32_t last = at == 0 ? w[0] : (at == 1 ? w[1] : (at == 2 ? w[2] : w[3]));
+            *reinterpret_cast<unsigned short*>(dst + at * 4) = static_cast<unsigned short>(last & 0xffffu);
+          }
+        }
 #ifdef FTB_EPI_NOSTORE
         if (false) {  // experiment build: staged but never stored
 #else

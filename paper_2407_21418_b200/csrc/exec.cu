@@ -87,21 +87,34 @@ void encode_map(CUtensorMap* m, const void* base, int64_t inner, int64_t rows, i
 // on B200 (tests/test_exec_gpu.py::test_dense_strided_output_untouched_padding):
 // stores clip the inner dimension at 16-byte granularity, so a row length N
 // that is not a multiple of 8 bf16 would clobber up to 7 elements past the
-// tensor edge — such problems keep the predicated st.global epilogue.
-bool encode_out_map(CUtensorMap* m, const ftb_gemm_desc& d) {
-  if (d.out_dtype != FTB_DT_BF16) return false;
-  if ((d.N * 2) % 16) return false;
-  if (reinterpret_cast<uintptr_t>(d.C) % 16 || (d.ldc * 2) % 16) return false;
+// tensor edge. Such problems (normal orientation, rows 16-B aligned, N >= 8)
+// get a map that ends at N8 = N rounded down to 8 — every box clips exactly
+// there — and the epilogue writes the last N - N8 (< 8) columns of each row
+// with element stores (kFlagTmaTail); returns 2 for that form. Otherwise
+// they keep the predicated st.global epilogue.
+int encode_out_map(CUtensorMap* m, const ftb_gemm_desc& d, bool swap) {
+  if (d.out_dtype != FTB_DT_BF16) return 0;
+  int64_t n_map = d.N;
+  if ((d.N * 2) % 16) {
+    const char* env = std::getenv("FTB_TMA_TAIL");
+    // small N: the < 8 scattered tail columns per row cost more than the
+    // predicated path saves (scores T = 15 / 23: 3.8 -> 4.0 us, T = 63 even)
+    const char* env_min = std::getenv("FTB_TMA_TAIL_MIN");
+    if (swap || d.N < (env_min ? std::atoi(env_min) : 48) || (env && env[0] == '0')) return 0;
+    n_map = d.N & ~int64_t(7);
+  }
+  if (reinterpret_cast<uintptr_t>(d.C) % 16 || (d.ldc * 2) % 16) return 0;
   const int64_t bs = d.batch > 1 ? d.c_batch_stride : d.M * d.ldc;
-  if ((bs * 2) % 16) return false;
-  cuuint64_t dims[3] = {static_cast<cuuint64_t>(d.N), static_cast<cuuint64_t>(d.M), static_cast<cuuint64_t>(d.batch)};
+  if ((bs * 2) % 16) return 0;
+  cuuint64_t dims[3] = {static_cast<cuuint64_t>(n_map), static_cast<cuuint64_t>(d.M), static_cast<cuuint64_t>(d.batch)};
   cuuint64_t strides[2] = {static_cast<cuuint64_t>(d.ldc * 2), static_cast<cuuint64_t>(bs * 2)};
   cuuint32_t box[3] = {32, 32, 1};
   cuuint32_t estr[3] = {1, 1, 1};
   CUresult r = get_encode()(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, d.C, dims, strides, box, estr,
                             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_64B,
                             CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-  return r == CUDA_SUCCESS;
+  if (r != CUDA_SUCCESS) return 0;
+  return n_map == d.N ? 1 : 2;
 }
 
 struct Region {
@@ -297,7 +310,7 @@ struct ExecImpl {
   DevProblem* d_problems = nullptr;
   DevWork* d_work = nullptr;
   DevMaps* d_maps = nullptr;
-  std::vector<uint8_t> tma_out;       // per problem: C store map usable
+  std::vector<uint8_t> tma_out;       // per problem: C store map usable (1), or up to N8 only (2, kFlagTmaTail)
   std::vector<int32_t> pack_depth;    // per problem: batch entries per TMA box (1 = no packing)
   std::vector<int32_t> pack_rows;     // per problem: lane box rows when packed
   TcWork* d_tcwork = nullptr;
@@ -489,7 +502,7 @@ static void build(ExecImpl& ex, const ftb_gemm_desc* probs, const ftb_program* p
           encode_map(&m.col[0], col_t, col_rows, d.K, d.batch, col_ld, col_bs, 64, 64);
         }
       }
-      ex.tma_out.push_back(encode_out_map(&m.out, d) ? 1 : 0);
+      ex.tma_out.push_back(static_cast<uint8_t>(encode_out_map(&m.out, d, swap)));
       m.epi.bias = d.bias;
       m.epi.bias_f32 = d.bias_dtype == FTB_DT_F32;
       m.epi.act = d.activation;
@@ -641,6 +654,22 @@ static void upload(ExecImpl& I) {
            (w.lane_len % 32 == 0 || w.lane0 + w.lane_len == lane_ext) &&
            (w.col_len % 32 == 0 || w.col0 + w.col_len == col_ext);
   };
+  // Contiguous rows (kFlagBulkStore): whole rows of a compact C, normal
+  // orientation, where TMA stores are not legal.
+  const char* env_bs = std::getenv("FTB_BULK_STORE");
+  const bool bulk_store_on = !(env_bs && env_bs[0] == '0');
+  auto bulk_ok = [&](const DevWork& w) {
+    const DevProblem& P = I.problems[w.problem];
+    return bulk_store_on && !P.swap && P.ldc == P.N && w.col0 == 0 && w.col_len == P.N;
+  };
+  auto store_flag = [&](bool tma, const DevWork& w) {
+    if (tma) {
+      const DevProblem& P = I.problems[w.problem];
+      const bool tail = I.tma_out[w.problem] == 2 && w.col0 + w.col_len == P.N;  // ends in the unmapped columns
+      return kFlagTmaStore | (tail ? kFlagTmaTail : 0u);
+    }
+    return bulk_ok(w) ? kFlagBulkStore : 0u;
+  };
   // CTA pairs: logical items of one problem/batch with the same column range
   // share the column operand; group them (in cost order) two by two. Off by
   // default: measured on B200 the pair kernel loses to the single-CTA kernel
@@ -676,7 +705,7 @@ static void upload(ExecImpl& I) {
       t.n_mma = static_cast<int32_t>(round_up(w.col_len, P.col_mn ? 128 : 32));
       t.num_kb = P.num_kb;
       t.batch = w.batch;
-      t.flags = flags_of(P) | (tma_ok(a) && tma_ok(w) ? kFlagTmaStore : 0u);
+      t.flags = flags_of(P) | (tma_ok(a) && tma_ok(w) && I.tma_out[w.problem] == 1 ? kFlagTmaStore : 0u);
       pairs.push_back(t);
       paired[it->second] = paired[i] = 1;
       open.erase(it);
@@ -715,7 +744,7 @@ static void upload(ExecImpl& I) {
       t.n_mma = depth * 64;  // the whole stacked MMA (entry e in columns [64e, 64e + 64))
       t.num_kb = P.num_kb;
       t.batch = w.batch;
-      t.flags = flags_of(P) | (ok ? kFlagTmaStore : 0u);
+      t.flags = flags_of(P) | store_flag(ok, w);
       t.pack = static_cast<uint32_t>(nb) | (static_cast<uint32_t>(depth) << 8) |
                (static_cast<uint32_t>(I.pack_rows[w.problem]) << 16);
       t.c_bs = static_cast<int32_t>(P.c_bs);
@@ -736,7 +765,7 @@ static void upload(ExecImpl& I) {
     t.n_mma = w.n_mma;
     t.num_kb = P.num_kb;
     t.batch = w.batch;
-    t.flags = flags_of(P) | (tma_ok(w) ? kFlagTmaStore : 0u);
+    t.flags = flags_of(P) | store_flag(tma_ok(w), w);
     max_n = std::max(max_n, w.n_mma);
     tw.push_back(t);
   }
@@ -881,6 +910,8 @@ static void upload(ExecImpl& I) {
         const bool col_mn = (t.flags & kFlagColMN) != 0;
         const int half = t.n_mma > 128 ? 128 : static_cast<int>(round_up((t.col_len + 1) / 2, 32));
         TcWork a = t, b = t;
+        a.flags &= ~(kFlagBulkStore | kFlagTmaTail);  // pieces no longer cover whole rows; only b ends at N
+        b.flags &= ~kFlagBulkStore;
         a.col_len = half;
         a.n_mma = t.n_mma > 128 ? 128 : half;
         b.col0 = t.col0 + half;

@@ -82,9 +82,21 @@ struct alignas(16) DevWork {
 //   partials meet in the fp32 workspace chunk by chunk (32 columns of one lane
 //   quadrant); the last split to publish a chunk sums it and stores C, so no
 //   split ever waits for another (no co-residency assumption; kernel_tc.cu).
+//   kFlagBulkStore: no TMA store map fits (C rows not a multiple of 16 B), but
+//   the item covers whole rows of a compact C (col0 = 0, col_len = N = ldc),
+//   so each epilogue warp's rows are one contiguous byte range: staged in
+//   shared memory in C's own layout and written by a 1-D bulk copy (plus
+//   element stores for the < 16 B head and tail) instead of scattered
+//   predicated stores.
 enum : uint32_t {
   kFlagSwap = 1u, kFlagLaneMN = 2u, kFlagColMN = 4u, kFlagOutF32 = 8u, kFlagTmaStore = 16u, kFlagSplitK = 32u,
-  kFlagEpiOp = 64u  // fused bias / activation: maps->epi
+  kFlagEpiOp = 64u,     // fused bias / activation: maps->epi
+  kFlagBulkStore = 128u,
+  // kFlagTmaTail: with kFlagTmaStore, C's row length N is not a multiple of 8
+  // bf16; the store map ends at N8 = N & ~7 (boxes clip exactly there) and the
+  // item, whose columns end at N, writes its last N - N8 columns per row with
+  // element stores
+  kFlagTmaTail = 256u
 };
 // Block-diagonal batch packing (short attention BMMs, exec.cu): `pack` holds
 // nb (entries in this item, bits 0-7), the TMA box depth (bits 8-15) and the

@@ -214,7 +214,7 @@ __device__ __forceinline__ void cluster_reduce(const TcConfig& cfg, const TcWork
   const int lane_base = quad * 32;
   if (lane_base >= it.lane_len) return;
   const bool swap = it.flags & kFlagSwap, f32 = it.flags & kFlagOutF32;
-  const bool tma = (it.flags & kFlagTmaStore) && !f32;
+  const bool tma = (it.flags & kFlagTmaStore) && !(it.flags & kFlagTmaTail) && !f32;
   const int s = cfg.cluster_split;
   const int rank = static_cast<int>(cluster_ctarank());
   float* tb = reinterpret_cast<float*>(region);
@@ -659,6 +659,10 @@ __global__ void __launch_bounds__(kEpi8 ? 384 : kTcThreads, 1)
         clo = egrp * half;
         clen = min(it.col_len, clo + half) - clo;
       }
+      // kFlagTmaTail: window-relative first column past the store map (N8)
+      const int tail0 = (it.flags & kFlagTmaTail) && clo + clen == it.col_len
+                            ? max(0, ((it.col0 + it.col_len) & ~7) - (it.col0 + clo))
+                            : (1 << 30);
       if (it.flags & kFlagSplitK) {
         split_epilogue<kCluster>(cfg, it, region, taddr, lane_base, swap, f32, release, reinterpret_cast<float*>(smem));
       } else if (clen <= 0) {
@@ -666,7 +670,8 @@ __global__ void __launch_bounds__(kEpi8 ? 384 : kTcThreads, 1)
       } else if (!it.pack) {
         epilogue_tile(region, ngrp, taddr + clo, lane_base < it.lane_len, tma, swap, f32, &it.maps->out, it.C, it.ldc,
                       it.lane0, it.lane_len, lane_base, it.col0 + clo, clen, it.batch, release,
-                      (it.flags & kFlagEpiOp) ? &it.maps->epi : nullptr);
+                      (it.flags & kFlagEpiOp) ? &it.maps->epi : nullptr,
+                      (it.flags & kFlagBulkStore) && clen == it.col_len, tail0);
       } else {
         // block-diagonal pack: this warp's lane quadrant belongs to entry e
         const int wpe = pack_lane_rows(it.pack) / 32;  // warps per entry
@@ -674,7 +679,8 @@ __global__ void __launch_bounds__(kEpi8 ? 384 : kTcThreads, 1)
         const bool active = e < pack_nb(it.pack) && r0 < it.lane_len;
         epilogue_tile(region, ngrp, taddr + e * 64 + clo, active, tma, swap, f32, &it.maps->out,
                       static_cast<char*>(it.C) + static_cast<size_t>(e) * it.c_bs * (f32 ? 4 : 2), it.ldc, 0,
-                      it.lane_len, r0, clo, clen, it.batch + e, release);
+                      it.lane_len, r0, clo, clen, it.batch + e, release, nullptr,
+                      (it.flags & kFlagBulkStore) && clen == it.col_len, tail0);
       }
       if (quad == 0 && lane == 0) trace_ev(cfg, local, 5);
     }

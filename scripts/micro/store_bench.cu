@@ -28,7 +28,7 @@ struct Maps { CUtensorMap s64; CUtensorMap s128; CUtensorMap s128w; CUtensorMap 
 __device__ __forceinline__ void named_bar(int id, int n) { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory"); }
 
 __global__ void __launch_bounds__(192, 1) store_kernel(const __grid_constant__ Maps maps, int items, int mode, int load,
-                                                      __nv_bfloat16* C, int64_t ldc, unsigned long long* out) {
+                                                      __nv_bfloat16* C, int64_t ldc, unsigned long long* out, int wrap) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = smem_raw + ((1024u - (smem_addr(smem_raw) & 1023u)) & 1023u);
   uint8_t* stage = smem;                 // 4 warps x 8 KiB (modes 0, 1, 4) or 2 x 16 KiB (mode 2)
@@ -65,7 +65,7 @@ __global__ void __launch_bounds__(192, 1) store_kernel(const __grid_constant__ M
     uint8_t* region = stage + warp * 8192;
     uint32_t ngrp = 0;
     for (int item = 0; item < items; ++item) {
-      const int64_t row0 = (static_cast<int64_t>(item) * gridDim.x + blockIdx.x) % 4096 * 128;  // distinct tiles, wraps in 1 GiB
+      const int64_t row0 = (static_cast<int64_t>(item) * gridDim.x + blockIdx.x) % wrap * 128;  // distinct tiles, wrap x 64 KiB footprint
       const int col0 = 0;
       for (int c0 = 0; c0 < 256; c0 += 64) {
         uint32_t r[32];
@@ -169,6 +169,7 @@ int main() {
   make(&m.s128w, c, ldc, rows, 64, 128, CU_TENSOR_MAP_SWIZZLE_128B);
   make(&m.ld, a, K, R, 64, 128, CU_TENSOR_MAP_SWIZZLE_128B);
   const int ctas = getenv("CTAS") ? atoi(getenv("CTAS")) : 148;
+  const int wrap = getenv("WRAP") ? atoi(getenv("WRAP")) : 4096;  // 256: 16 MiB footprint (L2-resident writes)
   const int smem = 32768 + 4 * 49152 + 1024 + 256;
   cudaFuncSetAttribute(store_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   const char* names[] = {"2KiB boxes {32x32} SW64 (current)", "4KiB boxes {64x32} SW128 per warp", "16KiB boxes {64x128} SW128 per CTA",
@@ -176,14 +177,14 @@ int main() {
   for (int items : {1, 16}) {
     for (int load : {0, 1}) {
       for (int mode : {0, 1, 2, 4}) {
-        store_kernel<<<ctas, 192, smem>>>(m, items, mode, load, (__nv_bfloat16*)c, ldc, out);
+        store_kernel<<<ctas, 192, smem>>>(m, items, mode, load, (__nv_bfloat16*)c, ldc, out, wrap);
         cudaDeviceSynchronize();
         cudaEvent_t e0, e1;
         cudaEventCreate(&e0);
         cudaEventCreate(&e1);
         cudaEventRecord(e0);
         const int reps = 20;
-        for (int r = 0; r < reps; ++r) store_kernel<<<ctas, 192, smem>>>(m, items, mode, load, (__nv_bfloat16*)c, ldc, out);
+        for (int r = 0; r < reps; ++r) store_kernel<<<ctas, 192, smem>>>(m, items, mode, load, (__nv_bfloat16*)c, ldc, out, wrap);
         cudaEventRecord(e1);
         cudaError_t e = cudaEventSynchronize(e1);
         float ms;
@@ -195,8 +196,8 @@ int main() {
         clk /= ctas;
         kbs /= ctas;
         const double bytes = 65536.0 * items;
-        printf("items %2d load %d  %-38s err=%d  %7.2f us/launch  per-SM store %6.1f B/clk (%6.0f clk/item)  loads %.0f KB/clk-ish %s\n",
-               items, load, names[mode], (int)e, ms * 1e3 / reps, bytes / clk, clk / items,
+        printf("wrap %4d items %2d load %d  %-38s err=%d  %7.2f us/launch  per-SM store %6.1f B/clk (%6.0f clk/item)  loads %.0f KB/clk-ish %s\n",
+               wrap, items, load, names[mode], (int)e, ms * 1e3 / reps, bytes / clk, clk / items,
                load ? kbs * 49152 / clk : 0.0, load ? "(48 KiB K blocks loaded per clk)" : "");
       }
     }

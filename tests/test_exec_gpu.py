@@ -359,3 +359,83 @@ def test_graph_replay_matches_eager_bitwise(cuda, case):
     torch.cuda.synchronize()
     assert not torch.isnan(eager.float()).any()
     assert torch.equal(C, eager)
+
+
+@pytest.mark.parametrize("case", ["s5", "s23", "s63", "s95", "s121", "s257", "dense_f32_odd"])
+def test_bulk_row_store_bitwise_and_bounds(cuda, monkeypatch, case):
+    """kFlagBulkStore (whole compact rows that no TMA map can describe: scores
+    with T % 8 != 0, fp32 outputs): the rows are written by a 1-D bulk copy
+    staged in C's own byte layout plus element stores for the unaligned head
+    and tail. C starts at an odd element offset of a guarded buffer (address
+    phase != 0 mod 16): every element of C is written, bit-identical to the
+    predicated path, and not one guard element is touched."""
+    from paper_2407_21418_b200.runtime import Planner, bmm_instance, dense_instance
+
+    g = torch.Generator(device="cpu").manual_seed(11)
+    guard = 37
+    if case.startswith("s"):
+        T, b = int(case[1:]), (384 if int(case[1:]) < 200 else 40)
+        A = (torch.rand(b, T, 64, generator=g) * 2 - 1).bfloat16().to(cuda)
+        B = (torch.rand(b, T, 64, generator=g) * 2 - 1).bfloat16().to(cuda)
+        shape, lay, inst, dt = (b, T, T), "nk", bmm_instance(b, T, T, 64), torch.bfloat16
+        ref = A.double() @ B.double().transpose(1, 2)
+        K = 64
+    else:
+        A = (torch.rand(3000, 64, generator=g) * 2 - 1).bfloat16().to(cuda)
+        B = (torch.rand(99, 64, generator=g) * 2 - 1).bfloat16().to(cuda)
+        shape, lay, inst, dt = (3000, 99), "nk", dense_instance(3000, 99, 64), torch.float32
+        ref = A.double() @ B.double().t()
+        K = 64
+    prog = Planner().plan([inst])[0].program
+    n = 1
+    for d in shape:
+        n *= d
+    outs = []
+    for bulk in ("0", "1"):
+        monkeypatch.setenv("FTB_BULK_STORE", bulk)
+        buf = torch.full((n + 2 * guard + 1,), float("nan"), dtype=dt, device=cuda)
+        C = buf[guard + 1: guard + 1 + n].view(shape)
+        ex = Executable([gemm_desc(A, B, C, lay)], [prog])
+        for _ in range(2):
+            ex.launch()
+        torch.cuda.synchronize()
+        assert torch.isnan(buf[: guard + 1].float()).all() and torch.isnan(buf[guard + 1 + n:].float()).all(), \
+            "a store landed outside C"
+        assert not torch.isnan(C.float()).any(), "an element of C was not written"
+        outs.append(C.clone())
+        ex.close()
+    assert torch.equal(outs[0], outs[1])
+    assert_close(outs[1], ref, K, case)
+
+
+@pytest.mark.parametrize("T", [9, 23, 50, 57, 60, 95, 121, 127, 255, 257])
+def test_tma_tail_store_padded_rows(cuda, monkeypatch, T):
+    """kFlagTmaTail: C rows padded to a multiple of 8 (16-B row stride, as the
+    attention outputs of the bench are allocated) but N = T % 8 != 0. The TMA
+    map ends at N rounded down to 8 and each row's last N % 8 columns are
+    element stores: bit-identical to the predicated path (FTB_TMA_TAIL=0),
+    every element written, the padding columns untouched."""
+    from paper_2407_21418_b200.runtime import Planner, bmm_instance
+
+    g = torch.Generator(device="cpu").manual_seed(T)
+    b = 384 if T < 200 else 40
+    Tp = (T + 7) // 8 * 8
+    A = (torch.rand(b, T, 64, generator=g) * 2 - 1).bfloat16().to(cuda)
+    B = (torch.rand(b, T, 64, generator=g) * 2 - 1).bfloat16().to(cuda)
+    ref = A.double() @ B.double().transpose(1, 2)
+    prog = Planner().plan([bmm_instance(b, T, T, 64)])[0].program
+    outs = []
+    for tail in ("0", "1"):
+        monkeypatch.setenv("FTB_TMA_TAIL", tail)
+        buf = torch.full((b, T, Tp), float("nan"), dtype=torch.bfloat16, device=cuda)
+        C = buf[:, :, :T]
+        ex = Executable([gemm_desc(A, B, C, "nk")], [prog])
+        ex.launch()
+        ex.launch()
+        torch.cuda.synchronize()
+        assert torch.isnan(buf[:, :, T:].float()).all(), "a store landed in the row padding"
+        assert not torch.isnan(C.float()).any(), "an element of C was not written"
+        outs.append(C.clone())
+        ex.close()
+    assert torch.equal(outs[0], outs[1])
+    assert_close(outs[1], ref, 64, f"T={T}")
