@@ -97,10 +97,11 @@ int encode_out_map(CUtensorMap* m, const ftb_gemm_desc& d, bool swap) {
   int64_t n_map = d.N;
   if ((d.N * 2) % 16) {
     const char* env = std::getenv("FTB_TMA_TAIL");
-    // small N: the < 8 scattered tail columns per row cost more than the
-    // predicated path saves (scores T = 15 / 23: 3.8 -> 4.0 us, T = 63 even)
+    // measured (profiles/r2be_tma_tail_min.txt): scores T = 39 / 45 5.1 /
+    // 5.3 -> 4.5 / 4.6 us, T = 95 / 121 8.8 / 9.6 -> 6.9 / 7.5 us; T < 16
+    // even, so those keep the predicated path
     const char* env_min = std::getenv("FTB_TMA_TAIL_MIN");
-    if (swap || d.N < (env_min ? std::atoi(env_min) : 48) || (env && env[0] == '0')) return 0;
+    if (swap || d.N < (env_min ? std::atoi(env_min) : 16) || (env && env[0] == '0')) return 0;
     n_map = d.N & ~int64_t(7);
   }
   if (reinterpret_cast<uintptr_t>(d.C) % 16 || (d.ldc * 2) % 16) return 0;
