@@ -204,7 +204,8 @@ __device__ __forceinline__ void split_epilogue(const TcConfig& cfg, const TcWork
 // On-chip split-K reduction (cfg.cluster_split > 1): CTA `rank` of the
 // cluster sums chunks rank, rank + s, ... of its lane quadrant over the s
 // partials held in the cluster's shared memories (distributed shared memory,
-// 16-B loads, two peers in flight; fixed split order: deterministic and
+// 16-B loads, only the chunk's column groups, all peers in flight for s = 4;
+// fixed split order: deterministic and
 // bit-identical to the workspace path at the same split count), applies the
 // fused epilogue op and stores C — through TMA store boxes when the item
 // allows it, else the coalesced predicated path.
@@ -227,6 +228,7 @@ __device__ __forceinline__ void cluster_reduce(const TcConfig& cfg, const TcWork
 #pragma unroll
     for (int e = 0; e < 32; ++e) v[e] = 0.f;
     const uint32_t mine = smem_addr(csmem + (static_cast<size_t>(ch * 4 + quad) << 10) + lane * 4);
+    const int ng = (min(32, it.col_len - ch * 32) + 3) >> 2;  // 4-column groups the chunk has
     if (s == 4) {
       // all four peers' loads in flight at once (one DSMEM round trip), then
       // the fixed-order sum
@@ -235,7 +237,7 @@ __device__ __forceinline__ void cluster_reduce(const TcConfig& cfg, const TcWork
       for (int p = 0; p < 4; ++p) {
         const uint32_t pa = mapa_shared(mine, static_cast<uint32_t>(p));
 #pragma unroll
-        for (int g = 0; g < 8; ++g) a[p][g] = ld_dsmem_v4(pa + g * 512);
+        for (int g = 0; g < 8; ++g) a[p][g] = g < ng ? ld_dsmem_v4(pa + g * 512) : make_float4(0.f, 0.f, 0.f, 0.f);
       }
 #pragma unroll
       for (int p = 0; p < 4; ++p)
@@ -254,8 +256,8 @@ __device__ __forceinline__ void cluster_reduce(const TcConfig& cfg, const TcWork
         float4 a[8], b[8];
 #pragma unroll
         for (int g = 0; g < 8; ++g) {
-          a[g] = ld_dsmem_v4(pa + g * 512);
-          b[g] = ld_dsmem_v4(pb + g * 512);
+          a[g] = g < ng ? ld_dsmem_v4(pa + g * 512) : make_float4(0.f, 0.f, 0.f, 0.f);
+          b[g] = g < ng ? ld_dsmem_v4(pb + g * 512) : make_float4(0.f, 0.f, 0.f, 0.f);
         }
 #pragma unroll
         for (int g = 0; g < 8; ++g) {
@@ -269,7 +271,7 @@ __device__ __forceinline__ void cluster_reduce(const TcConfig& cfg, const TcWork
         const uint32_t pa = mapa_shared(mine, static_cast<uint32_t>(p));
         float4 a[8];
 #pragma unroll
-        for (int g = 0; g < 8; ++g) a[g] = ld_dsmem_v4(pa + g * 512);
+        for (int g = 0; g < 8; ++g) a[g] = g < ng ? ld_dsmem_v4(pa + g * 512) : make_float4(0.f, 0.f, 0.f, 0.f);
 #pragma unroll
         for (int g = 0; g < 8; ++g) {
           v[4 * g] += a[g].x;
@@ -699,6 +701,8 @@ __global__ void __launch_bounds__(kEpi8 ? 384 : kTcThreads, 1)
   }
 
   tc_fence_before();
+  TcWork cl_it;  // the reduce's work record, fetched before the barrier (off the tail)
+  if (kCluster && warp >= 2 && static_cast<int>(blockIdx.x) < n_work) cl_it = load_work(work, blockIdx.x);
   __syncthreads();
   if (kCluster) {  // one item per CTA: reduce the cluster's split-K partials on chip
 #ifdef FTB_TRACE
@@ -709,7 +713,7 @@ __global__ void __launch_bounds__(kEpi8 ? 384 : kTcThreads, 1)
     if (threadIdx.x == 64 && cfg.trace) cfg.trace[blockIdx.x * kTracePerCta + kTraceItems * kTraceEvents + 121] = clock64();
 #endif
     if (warp >= 2 && static_cast<int>(blockIdx.x) < n_work)
-      cluster_reduce(cfg, load_work(work, blockIdx.x), reinterpret_cast<uint8_t*>(epi_buf) + (warp & 3) * kEpiWarpBytes,
+      cluster_reduce(cfg, cl_it, reinterpret_cast<uint8_t*>(epi_buf) + (warp & 3) * kEpiWarpBytes,
                      reinterpret_cast<float*>(smem), warp & 3);
 #ifdef FTB_TRACE
     if (threadIdx.x == 64 && cfg.trace) cfg.trace[blockIdx.x * kTracePerCta + kTraceItems * kTraceEvents + 122] = clock64();  // debug (clk): warp 2 done reducing

@@ -98,6 +98,12 @@ for spec in os.environ.get("SHAPES", "bmm 384 5 5 64 nk;bmm 384 100 100 64 nk;de
             d = np.diff(c, axis=1)
             print(f"     cluster clk: sync1 p50 {np.median(d[:, 0]):.0f} max {d[:, 0].max():.0f} | reduce p50 "
                   f"{np.median(d[:, 1]):.0f} max {d[:, 1].max():.0f} | sync2 p50 {np.median(d[:, 2]):.0f} max {d[:, 2].max():.0f}")
+            x = kb[:, 62:64, :].reshape(len(kb), 4).astype(np.int64)  # 124 summed, 125 stored, 126 entry
+            red = (x[:, 2] > 0) & (x[:, 0] > 0)
+            if red.any():
+                r0 = c[red, 1]
+                print(f"     reducing CTAs: entry-after-sync1 {np.median(x[red, 2] - r0):.0f} | loads+sum {np.median(x[red, 0] - x[red, 2]):.0f}"
+                      f" | stage+store issue {np.median(x[red, 1] - x[red, 0]):.0f} | rest {np.median(c[red, 2] - x[red, 1]):.0f} clk")
         if os.environ.get("KB"):
             kbr = np.where(kb > 0, kb.astype(np.int64) - t0, -1) / 1e3
             print("     kb issue-stamp:", " ".join(f"{v:.2f}" for v in kbr[0, :8, 0]), "| mma saw:",

@@ -58,7 +58,7 @@ __global__ void __launch_bounds__(128, 1) mma_kernel(const __grid_constant__ Map
       if (it < 16) tiss[it] = clock64() - t0;
       if (++ps == S) { ps = 0; ph ^= 1; }
     }
-  } else if (warp == 1 && mma_on == 7) {
+  } else if (warp == 1 && mma_on >= 7) {  // 7: converged elect.sync issue, one accumulator; 8: two alternating; 9: four
     const uint32_t tm = __shfl_sync(0xffffffffu, tmem, 0);
     const uint32_t idesc = idesc_bf16_f32(PAIR ? 256 : 128, N, 0, 0);
     const uint32_t base = smem_addr(smem);
@@ -68,12 +68,12 @@ __global__ void __launch_bounds__(128, 1) mma_kernel(const __grid_constant__ Map
 #pragma unroll
       for (int kk = 0; kk < 4; ++kk) {
         const uint64_t ad = umma_desc_sw128(la + kk * 32, 16, 1024), bd = umma_desc_sw128(ca + kk * 32, 16, 1024);
-        const uint32_t acc = (it | kk) != 0;
+        const uint32_t acc = mma_on == 7 ? (it | kk) != 0 : it != 0;
         asm volatile(
             "{\n.reg .pred p, q;\n"
             "elect.sync _|p, 0xffffffff;\n"
             "setp.ne.b32 q, %4, 0;\n"
-            "@p tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, q;\n}\n" ::"r"(tm),
+            "@p tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, q;\n}\n" ::"r"(tm + (mma_on == 8 ? (kk & 1) * N : (mma_on == 9 ? kk * N : 0))),
             "l"(ad), "l"(bd), "r"(idesc), "r"(acc)
             : "memory");
       }
