@@ -29,7 +29,7 @@
 
 namespace ftb {
 
-cudaError_t launch_tc(const TcWork*, int32_t, int32_t, TcConfig, cudaStream_t);
+cudaError_t launch_tc(const TcWork*, int32_t, int32_t, TcConfig, const DevMaps*, cudaStream_t);
 cudaError_t launch_tc2(const TcPair*, int32_t, int32_t, TcConfig, cudaStream_t);
 int tc_smem_bytes(const TcConfig& cfg);
 cudaError_t launch_ffma(const DevProblem*, const DevWork*, int32_t, int32_t, cudaStream_t, bool);
@@ -1090,6 +1090,8 @@ static void upload(ExecImpl& I) {
   {
     const char* env_pf = std::getenv("FTB_L2_PREFETCH");
     I.cfg.l2_prefetch = (env_pf && env_pf[0] == '0') ? 0 : 1;
+    const char* env_pm = std::getenv("FTB_PARAM_MAPS");
+    I.cfg.param_maps = (I.maps.size() == 1 && !(env_pm && env_pm[0] == '0')) ? 1 : 0;
   }
   I.cfg.split_ws = I.d_split_ws;
   I.cfg.split_cnt = I.d_split_cnt;
@@ -1173,7 +1175,8 @@ ftb_status ftb_exec_launch(ftb_exec* ex, void* stream) {
     if (e == cudaSuccess && I.info.kernel == 0 && I.n_pairs)
       e = ftb::launch_tc2(I.d_tcpairs, static_cast<int32_t>(I.n_pairs), static_cast<int32_t>(I.ctas2), I.cfg2, s);
     if (e == cudaSuccess && I.info.kernel == 0 && I.n_singles)
-      e = ftb::launch_tc(I.d_tcwork, static_cast<int32_t>(I.n_singles), static_cast<int32_t>(I.ctas1), I.cfg, s);
+      e = ftb::launch_tc(I.d_tcwork, static_cast<int32_t>(I.n_singles), static_cast<int32_t>(I.ctas1), I.cfg,
+                         I.maps.empty() ? nullptr : I.maps.data(), s);
     if (e != cudaSuccess) throw ftb::cuda_error(std::string("kernel launch: ") + cudaGetErrorString(e));
     if (capturing) I.captured = true;
     if (!capturing) {  // destroy frees the table only after this launch (exec.cu ~ExecImpl)

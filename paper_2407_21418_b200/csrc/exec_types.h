@@ -155,6 +155,7 @@ struct TcConfig {
   int32_t cluster_split;      // > 1: split-K partials reduced on chip across a cluster of this many CTAs
   int32_t epi8;               // 1: eight epilogue warps (two groups on alternate items), 320 threads
   int32_t l2_prefetch;        // 1: L2-prefetch the first item's operands before griddepcontrol.wait
+  int32_t param_maps;         // 1: single-problem table, descriptors in the kernel parameter (see kernel_tc.cu with_maps)
 };
 constexpr int kTraceItems = 16;   // items traced per CTA
 constexpr int kTraceEvents = 6;   // see kernel_tc.cu

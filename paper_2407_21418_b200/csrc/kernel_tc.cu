@@ -76,6 +76,17 @@ __device__ __forceinline__ TcWork bcast_work(uint32_t mine) {
   return it;
 }
 
+// Single-problem tables pass the problem's TMA descriptors as a
+// __grid_constant__ kernel parameter (cfg.param_maps): TMA loads / stores and
+// descriptor prefetches then read them from the launch's parameter bank
+// instead of fetching the table copy from global memory after the work
+// record arrives — one dependent global round trip off every launch's
+// critical path.
+__device__ __forceinline__ TcWork with_maps(TcWork t, const TcConfig& cfg, const DevMaps* pm) {
+  if (cfg.param_maps) t.maps = pm;
+  return t;
+}
+
 // Split-K epilogue for one warp (lane quadrant): publish the fp32 partial of
 // this split to the workspace and count its arrival per 32-column chunk; the
 // split completing a chunk sums all partials of it (fixed split order, so the
@@ -321,7 +332,7 @@ __device__ __forceinline__ void cluster_reduce(const TcConfig& cfg, const TcWork
 // common kernel carries none of their code.
 template <int S, bool kCluster, bool kEpi8>
 __global__ void __launch_bounds__(kEpi8 ? 384 : kTcThreads, 1)
-    ftb_tc_kernel(const TcWork* __restrict__ work, int32_t n_work, TcConfig cfg) {
+    ftb_tc_kernel(const TcWork* __restrict__ work, int32_t n_work, TcConfig cfg, const __grid_constant__ DevMaps pmaps) {
   extern __shared__ uint8_t smem_raw[];
   // 1024-B aligned base, derived by pointer arithmetic on the __shared__ array
   // so the compiler keeps the shared state space: every staging / transpose
@@ -393,8 +404,8 @@ __global__ void __launch_bounds__(kEpi8 ? 384 : kTcThreads, 1)
 #endif
     TcWork cur, nxt;
     uint32_t pend = 0;  // raw word of the record two items ahead
-    if (static_cast<int>(blockIdx.x) < n_work) cur = bcast_work(fetch_work_word(work, blockIdx.x));
-    if (static_cast<int>(blockIdx.x) + G < n_work) nxt = bcast_work(fetch_work_word(work, blockIdx.x + G));
+    if (static_cast<int>(blockIdx.x) < n_work) cur = with_maps(bcast_work(fetch_work_word(work, blockIdx.x)), cfg, &pmaps);
+    if (static_cast<int>(blockIdx.x) + G < n_work) nxt = with_maps(bcast_work(fetch_work_word(work, blockIdx.x + G)), cfg, &pmaps);
     if (static_cast<int>(blockIdx.x) + 2 * G < n_work) pend = fetch_work_word(work, blockIdx.x + 2 * G);
     if (lane == 0 && static_cast<int>(blockIdx.x) < n_work) {
       tma_prefetch_desc(&cur.maps->lane);
@@ -525,7 +536,7 @@ __global__ void __launch_bounds__(kEpi8 ? 384 : kTcThreads, 1)
       c_item += clock64() - ci;
 #endif
       cur = nxt;
-      if (w + 2 * G < n_work) nxt = bcast_work(pend);
+      if (w + 2 * G < n_work) nxt = with_maps(bcast_work(pend), cfg, &pmaps);
       if (w + 3 * G < n_work) pend = fetch_work_word(work, w + 3 * G);
     }
 #ifdef FTB_PROD_PROFILE
@@ -629,10 +640,10 @@ __global__ void __launch_bounds__(kEpi8 ? 384 : kTcThreads, 1)
 #endif
     TcWork nxt;
     const int w0 = static_cast<int>(blockIdx.x) + (csplit ? 0 : egrp * G);
-    if (w0 < n_work) nxt = load_work(work, w0);
+    if (w0 < n_work) nxt = with_maps(load_work(work, w0), cfg, &pmaps);
     for (int w = w0; w < n_work; w += step * G, local += step) {
       const TcWork it = nxt;
-      if (w + step * G < n_work) nxt = load_work(work, w + step * G);
+      if (w + step * G < n_work) nxt = with_maps(load_work(work, w + step * G), cfg, &pmaps);
       const uint32_t slot = local % cfg.n_acc;
       const uint32_t use = local / cfg.n_acc;
       const bool swap = it.flags & kFlagSwap, f32 = it.flags & kFlagOutF32;
@@ -702,7 +713,7 @@ __global__ void __launch_bounds__(kEpi8 ? 384 : kTcThreads, 1)
 
   tc_fence_before();
   TcWork cl_it;  // the reduce's work record, fetched before the barrier (off the tail)
-  if (kCluster && warp >= 2 && static_cast<int>(blockIdx.x) < n_work) cl_it = load_work(work, blockIdx.x);
+  if (kCluster && warp >= 2 && static_cast<int>(blockIdx.x) < n_work) cl_it = with_maps(load_work(work, blockIdx.x), cfg, &pmaps);
   __syncthreads();
   if (kCluster) {  // one item per CTA: reduce the cluster's split-K partials on chip
 #ifdef FTB_TRACE
@@ -740,31 +751,36 @@ int tc_smem_bytes(const TcConfig& cfg) {
 
 template <int S, bool kCluster, bool kEpi8>
 static cudaError_t launch_tc_sk(const TcWork* work, int32_t n_work, int32_t n_ctas, TcConfig cfg,
-                                cudaStream_t stream) {
+                                const DevMaps& pmaps, cudaStream_t stream) {
   cudaError_t e = configure_smem_once<ftb_tc_kernel<S, kCluster, kEpi8>>(232448);
   if (e != cudaSuccess) return e;
   return launch_pdl_cluster(ftb_tc_kernel<S, kCluster, kEpi8>, n_ctas, kEpi8 ? kTcThreadsEpi8 : kTcThreads,
-                            tc_smem_bytes(cfg), kCluster ? cfg.cluster_split : 1, stream, work, n_work, cfg);
+                            tc_smem_bytes(cfg), kCluster ? cfg.cluster_split : 1, stream, work, n_work, cfg, pmaps);
 }
 template <int S>
 static cudaError_t launch_tc_s(const TcWork* work, int32_t n_work, int32_t n_ctas, TcConfig cfg,
-                               cudaStream_t stream) {
-  if (cfg.cluster_split > 1) return launch_tc_sk<S, true, false>(work, n_work, n_ctas, cfg, stream);
-  if (cfg.epi8) return launch_tc_sk<S, false, true>(work, n_work, n_ctas, cfg, stream);
-  return launch_tc_sk<S, false, false>(work, n_work, n_ctas, cfg, stream);
+                               const DevMaps& pmaps, cudaStream_t stream) {
+  if (cfg.cluster_split > 1) return launch_tc_sk<S, true, false>(work, n_work, n_ctas, cfg, pmaps, stream);
+  if (cfg.epi8) return launch_tc_sk<S, false, true>(work, n_work, n_ctas, cfg, pmaps, stream);
+  return launch_tc_sk<S, false, false>(work, n_work, n_ctas, cfg, pmaps, stream);
 }
 
-cudaError_t launch_tc(const TcWork* work, int32_t n_work, int32_t n_ctas, TcConfig cfg,
+// param_maps: the descriptors of a single-problem table (host copy), passed
+// as a kernel parameter when cfg.param_maps is set; ignored otherwise.
+cudaError_t launch_tc(const TcWork* work, int32_t n_work, int32_t n_ctas, TcConfig cfg, const DevMaps* param_maps,
                       cudaStream_t stream) {
   if (n_work == 0) return cudaSuccess;
+  static const DevMaps none{};
+  const DevMaps& pm = (cfg.param_maps && param_maps) ? *param_maps : none;
+  if (cfg.param_maps && !param_maps) return cudaErrorInvalidValue;
   switch (cfg.stages) {
-    case 2: return launch_tc_s<2>(work, n_work, n_ctas, cfg, stream);
-    case 3: return launch_tc_s<3>(work, n_work, n_ctas, cfg, stream);
-    case 4: return launch_tc_s<4>(work, n_work, n_ctas, cfg, stream);
-    case 5: return launch_tc_s<5>(work, n_work, n_ctas, cfg, stream);
-    case 6: return launch_tc_s<6>(work, n_work, n_ctas, cfg, stream);
-    case 7: return launch_tc_s<7>(work, n_work, n_ctas, cfg, stream);
-    case 8: return launch_tc_s<8>(work, n_work, n_ctas, cfg, stream);
+    case 2: return launch_tc_s<2>(work, n_work, n_ctas, cfg, pm, stream);
+    case 3: return launch_tc_s<3>(work, n_work, n_ctas, cfg, pm, stream);
+    case 4: return launch_tc_s<4>(work, n_work, n_ctas, cfg, pm, stream);
+    case 5: return launch_tc_s<5>(work, n_work, n_ctas, cfg, pm, stream);
+    case 6: return launch_tc_s<6>(work, n_work, n_ctas, cfg, pm, stream);
+    case 7: return launch_tc_s<7>(work, n_work, n_ctas, cfg, pm, stream);
+    case 8: return launch_tc_s<8>(work, n_work, n_ctas, cfg, pm, stream);
     default: return cudaErrorInvalidValue;
   }
 }
