@@ -978,6 +978,46 @@ static void upload(ExecImpl& I) {
       }
     }
   }
+  // Overflow split: a table of n > P plain items (P = SMs) whose last round
+  // holds only r = n mod P <= P / 2 items runs that round on r CTAs, so a 5 %
+  // larger shape can take 40 % longer (C1 qkv M = 2048: 144 items 10.0 us,
+  // M = 2144: 153 items 13.8 us). The r cheapest items (the table is
+  // cost-sorted, they are last) are cut into 64-column pieces (128 when
+  // 4r > P), which the round-robin deals to the first CTAs after their full
+  // items: the last round shrinks to a narrow item's K loop (M = 2144: 11.1
+  // us; qkv M = 2496 / 2592, FFN1 M = 1728-2144: -11 to -17 %,
+  // profiles/r2bh_overflow_split.txt). Same per-element K order: bit-identical.
+  {
+    const char* env_ov = std::getenv("FTB_OVERFLOW_SPLIT");
+    const int64_t n = static_cast<int64_t>(tw.size()), P = sms_all;
+    const int64_t r = n > P ? n % P : 0;  // items of the last, partial round
+    bool ok = !(env_ov && env_ov[0] == '0') && !wide_split && !pairing && I.cfg.cluster_split <= 1 && r > 0 &&
+              2 * r <= P;
+    const int w = 4 * r <= P ? 64 : 128;
+    for (int64_t i = 0; ok && i < n; ++i) {
+      const TcWork& t = tw[static_cast<size_t>(i)];
+      if (t.flags & kFlagSplitK) ok = false;  // workspace split-K tables keep their layout
+      if (i >= n - r && (t.pack || (t.flags & kFlagColMN) || t.n_mma <= w || t.col_len <= w)) ok = false;
+    }
+    if (ok) {
+      std::vector<TcWork> ov;
+      ov.reserve(static_cast<size_t>(n + 3 * r));
+      for (int64_t i = 0; i < n - r; ++i) ov.push_back(tw[static_cast<size_t>(i)]);
+      for (int64_t i = n - r; i < n; ++i) {
+        const TcWork& t = tw[static_cast<size_t>(i)];
+        for (int c = 0; c < t.col_len; c += w) {
+          TcWork u = t;
+          u.col0 = t.col0 + c;
+          u.col_len = std::min(w, t.col_len - c);
+          u.n_mma = static_cast<int32_t>(round_up(u.col_len, 32));
+          u.flags &= ~kFlagBulkStore;
+          if (c + w < t.col_len) u.flags &= ~kFlagTmaTail;  // only the last piece ends at N
+          ov.push_back(u);
+        }
+      }
+      tw.swap(ov);
+    }
+  }
   // Interleave long (MMA/TMA-bound, e.g. Dense) and short (latency-bound,
   // e.g. attention BMM) items in rounds of one item per CTA, so each CTA
   // alternates them: a short item's load -> MMA -> epilogue chain then hides

@@ -439,3 +439,37 @@ def test_tma_tail_store_padded_rows(cuda, monkeypatch, T):
         ex.close()
     assert torch.equal(outs[0], outs[1])
     assert_close(outs[1], ref, 64, f"T={T}")
+
+
+@pytest.mark.parametrize("M,N,K,grows", [(2144, 2304, 768, True), (1728, 3072, 768, True), (3200, 3072, 768, True),
+                                         (2144, 2312, 136, False)])
+def test_overflow_split_bitwise(cuda, monkeypatch, M, N, K, grows):
+    """Overflow split (exec.cu): a table whose last round holds r <= P / 2
+    items cuts those into 64/128-column pieces. Bit-identical to the unsplit
+    table (same per-element K order), per-element close to fp64, and the
+    table really grows (kernel items > logical items). N = 2312 (not a
+    multiple of 8, TMA tail stores): its cheapest, last-round items are the
+    8-column edge pieces, already narrow, so nothing is split."""
+    from paper_2407_21418_b200.runtime import Planner, dense_instance
+
+    g = torch.Generator(device="cpu").manual_seed(M + N)
+    A = (torch.rand(M, K, generator=g) * 2 - 1).bfloat16().to(cuda)
+    B = (torch.rand(N, K, generator=g) * 2 - 1).bfloat16().to(cuda)
+    ref = A.double() @ B.double().t()
+    prog = Planner().plan([dense_instance(M, N, K)])[0].program
+    Np = (N + 7) // 8 * 8
+    outs, items = [], []
+    for ov in ("0", "1"):
+        monkeypatch.setenv("FTB_OVERFLOW_SPLIT", ov)
+        buf = torch.full((M, Np), float("nan"), dtype=torch.bfloat16, device=cuda)
+        C = buf[:, :N]
+        ex = Executable([gemm_desc(A, B, C, "nk")], [prog])
+        ex.launch()
+        torch.cuda.synchronize()
+        assert torch.isnan(buf[:, N:].float()).all()
+        outs.append(C.clone())
+        items.append(ex.config()["n_singles"])
+        ex.close()
+    assert torch.equal(outs[0], outs[1])
+    assert (items[1] > items[0]) == grows, items
+    assert_close(outs[1], ref, K, f"M{M} N{N} K{K}")
