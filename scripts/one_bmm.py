@@ -12,6 +12,8 @@ Bt = (torch.randn(b, K, pad(N), device="cuda").bfloat16()[:, :, :N] if lay == "k
       else torch.randn(b, N, pad(K), device="cuda").bfloat16()[:, :, :K])
 npad = (N + 7) // 8 * 8
 C = torch.full((b, M, npad), float("nan"), device="cuda").bfloat16()[:, :, :N]
+if os.environ.get("COMPACT"):  # C rows not padded to 16 B: the bulk row-store path
+    C = torch.full((b, M, N), float("nan"), device="cuda").bfloat16()
 rec = Planner().plan([bmm_instance(b, M, N, K)])[0]
 ex = Executable([gemm_desc(A, Bt, C, lay)], [rec.program], (A, Bt, C))
 print(rec.describe()["parts"], rec.describe()["tau"], ex.info.n_work, ex.info.n_ctas, ex.config()["single"], flush=True)

@@ -1,6 +1,7 @@
 # compute-sanitizer memcheck + racecheck over every kernel instantiation / lowering path:
 # common kernel (swap-AB ragged pieces, MN-major B), on-chip cluster split-K (s=2 and s=4),
-# global-workspace split-K, eight-warp epilogue (natural BMM table and forced Dense), CTA-pair kernel.
+# global-workspace split-K, eight-warp epilogue (natural BMM table and forced Dense), CTA-pair kernel;
+# round 2: TMA tail stores, bulk row stores, overflow split, 32-column pieces with param-space descriptors.
 export PYTHONUNBUFFERED=1
 OUT=${OUT:-gpurun_out/sanitize.txt}
 : > $OUT
@@ -21,4 +22,8 @@ SCRIPT=scripts/one_dense.py run "global-workspace split-K" FTB_SPLIT_CLUSTER=0 M
 SCRIPT=scripts/one_dense.py run "eight-warp epilogue (forced), Dense" FTB_EPI8=1 M=1000 N=2304 K=512 ORIENT=-1
 SCRIPT=scripts/one_bmm.py run "eight-warp epilogue (natural), BMM 192x64x64x64" B=192 M=64 N=64 K=64
 SCRIPT=scripts/one_dense.py run "large Dense (CTA-pair candidate)" M=2048 N=3072 K=768 ORIENT=-1
+SCRIPT=scripts/one_bmm.py run "TMA tail stores, scores T=95 (padded rows)" B=384 M=95 N=95 K=64 LAYOUT=nk
+SCRIPT=scripts/one_bmm.py run "bulk row stores, scores T=95 (compact rows)" COMPACT=1 B=64 M=95 N=95 K=64 LAYOUT=nk
+SCRIPT=scripts/one_dense.py run "overflow split (153 items)" M=2144 N=2304 K=768 ORIENT=-1
+SCRIPT=scripts/one_dense.py run "32-column pieces, param-space TMA descriptors" M=160 N=768 K=768 ORIENT=-1
 cat $OUT
