@@ -518,7 +518,67 @@ static void build(ExecImpl& ex, const ftb_gemm_desc* probs, const ftb_program* p
     const int64_t col_max = ffma ? 64 : kMaxN;
     const int64_t gran = P.col_mn ? 64 : 16;
     const size_t first_item = items.size();
+    if (ffma) {
+      // FFMA items are unions of whole uKernel rectangles. The plan's
+      // rectangles form a grid (the parts share every non-tau tile,
+      // combine.py:118-123): i cells x j cells per batch entry. Consecutive
+      // cells are merged along each axis up to the kernel's 64 x 64 CTA tile
+      // (a cell larger than 64 is cut as before), so the small uKernels the
+      // FFMA descriptor picks (C0: 3 x 32 ... 30 x 32) no longer leave most of
+      // a CTA's 256 threads idle; every output element is still one
+      // sequential-K FFMA chain, so the result is bit-identical.
+      auto cuts = [&](int ax, int64_t extent) {
+        std::vector<int64_t> c;
+        for (const Region& r : regs) c.push_back(r.lo[ax]);
+        c.push_back(extent);
+        std::sort(c.begin(), c.end());
+        c.erase(std::unique(c.begin(), c.end()), c.end());
+        return c;
+      };
+      auto group = [&](const std::vector<int64_t>& c, int64_t maxlen, std::vector<Piece>& out) {
+        out.clear();
+        std::vector<Piece> tmp;
+        int64_t gs = c.front(), gl = 0;
+        for (size_t k = 0; k + 1 < c.size(); ++k) {
+          const int64_t len = c[k + 1] - c[k];
+          if (len > maxlen) {
+            if (gl) out.push_back({gs, gl});
+            split(c[k], c[k + 1], maxlen, tmp, 1);
+            out.insert(out.end(), tmp.begin(), tmp.end());
+            gs = c[k + 1];
+            gl = 0;
+            continue;
+          }
+          if (gl + len > maxlen) {
+            out.push_back({gs, gl});
+            gs = c[k];
+            gl = 0;
+          }
+          gl += len;
+        }
+        if (gl) out.push_back({gs, gl});
+      };
+      group(cuts(ib, d.M), lane_max, lp);
+      group(cuts(ib + 1, d.N), col_max, cp);
+      for (int64_t b = 0; b < (ib ? d.batch : 1); ++b)
+        for (auto& L : lp)
+          for (auto& Cc : cp) {
+            DevWork w;
+            w.problem = p;
+            w.batch = static_cast<int32_t>(b);
+            w.lane0 = static_cast<int32_t>(L.start);
+            w.col0 = static_cast<int32_t>(Cc.start);
+            w.lane_len = static_cast<int32_t>(L.len);
+            w.col_len = static_cast<int32_t>(Cc.len);
+            w.n_mma = static_cast<int32_t>(Cc.len);
+            w.aux = 0;
+            const int64_t cells = static_cast<int64_t>(P.num_kb) * L.len * Cc.len;
+            items.push_back({cells, w});
+            ex.info.mma_flops += 2 * cells * kBlockK;
+          }
+    }
     for (const Region& r : regs) {
+      if (ffma) break;
       const int64_t b0 = ib ? r.lo[0] : 0, b1 = ib ? r.hi[0] : 1;
       const int64_t ilo = r.lo[ib], ihi = r.hi[ib], jlo = r.lo[ib + 1], jhi = r.hi[ib + 1];
       // j is C's innermost dimension (and B's when B is [K, N]): pieces along
@@ -590,11 +650,12 @@ static void build(ExecImpl& ex, const ftb_gemm_desc* probs, const ftb_program* p
   int sms = device_sms();
   if (sms <= 0) sms = 148;
   ex.info.n_ctas = std::min<int64_t>(ex.info.n_work, ffma ? 4 * sms : sms);
-  if (ffma) {  // the FFMA kernel's 16-B copies need 16-B aligned operand rows
+  if (ffma) {  // the FFMA kernel's 16-B copies need 16-B aligned operand rows (and item column origins)
     bool vec = true;
     for (const DevProblem& P : ex.problems)
       vec = vec && reinterpret_cast<uintptr_t>(P.A) % 16 == 0 && reinterpret_cast<uintptr_t>(P.B) % 16 == 0 &&
             P.lda % 4 == 0 && P.ldb % 4 == 0 && (P.batch == 1 || (P.a_bs % 4 == 0 && P.b_bs % 4 == 0));
+    for (const DevWork& w : ex.work) vec = vec && w.col0 % 4 == 0;
     ex.ffma_vec = vec;
   }
   if (ex.info.n_work > INT32_MAX) throw input_error("tile table too large", "work");
