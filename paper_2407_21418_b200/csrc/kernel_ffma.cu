@@ -1,20 +1,22 @@
 // kernel_ffma.cu — K2: fp32 FFMA executor for the validation mode (config 0:
 // fp32 Dense, N=K=768; any fp32 Dense / BMM). Same tile-schedule table as
-// K1: each work item is an output rectangle (<= 64 x 64 after lowering splits
-// a uKernel tile). K streams through a 3-stage shared-memory ring of 32-wide
-// slices filled by cp.async — only the item's own rows / columns (the
-// uKernels the FFMA descriptor picks are small, e.g. 29 x 32, PAPER.md
-// Fig. 8), the K tail zero-filled, B [K, N] rows in 16-B copies when aligned —
-// so two slices are in flight behind the one being multiplied. Both slices are
-// stored k-major, so every thread reads its 4 x 4 register tile's operands
-// with two 16-B shared loads per 16 FFMAs. At fp32 the accumulation order is plain
-// sequential-K FFMA, which is what the 1e-5 tolerance is set against.
+// K1: each work item is an output rectangle of at most 64 x 64 — whole plan
+// uKernel rectangles merged (exec.cu; the FFMA descriptor's uKernels are
+// small, e.g. 3 x 32 ... 30 x 32, Fig. 8). K streams through a
+// 6-stage shared-memory ring of 32-wide slices filled by cp.async — only the
+// item's own rows / columns, the K tail zero-filled; A rows (K-contiguous)
+// and B [K, N] rows in 16-B copies when aligned — so five slices are in
+// flight behind the one being multiplied. A is staged [row][k], B [k][n]:
+// per four K steps a thread reads its 4 x 4 register tile's operands with
+// eight 16-B shared loads for 64 FFMAs. At fp32 the accumulation order is
+// plain sequential-K FFMA, which is what the 1e-5 tolerance is set against.
 // Orientation is always lanes = i, columns = j.
 //
 // Round 2 (scripts/c0_time.py, C0 M = 512, L2-cold chain): round 1's kernel
 // issued sixteen 4-B load + store round trips per thread and slice for the
-// whole 64 x 64 tile whatever the item's size: 164 us (cuBLAS fp32 22 us);
-// the inner loop's eight 4-B shared loads per 16 FFMAs capped it as much.
+// whole 64 x 64 tile whatever the item's size: 164 us; one CTA per uKernel
+// rectangle, 4-B A copies: 115 us; merged rectangles + this kernel: 37.7 us
+// (cuBLAS fp32 22.4 us; profiles/r2bk_c0_ffma_merge.txt).
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
 
@@ -26,9 +28,10 @@ namespace ftb {
 constexpr int kFfmaTile = 64;
 constexpr int kFfmaK = 32;
 constexpr int kFfmaThreads = 256;
-constexpr int kFfmaStages = 3;
+constexpr int kFfmaStages = 6;
 constexpr int kFfmaPer = kFfmaTile * kFfmaK / kFfmaThreads;  // 8 elements of A (and of B) per thread and slice
 constexpr int kFfmaLdN = kFfmaTile + 4;                       // padded row of a [k][n] slice
+constexpr int kFfmaLdK = kFfmaK + 4;                          // padded row of an A [row][k] slice (144 B)
 
 // 4-B global -> shared copy; src_bytes = 0 writes a zero
 __device__ __forceinline__ void cp_async4(float* dst, const float* src, bool valid) {
@@ -51,9 +54,11 @@ __global__ void __launch_bounds__(kFfmaThreads)
     ftb_ffma_kernel(const DevProblem* __restrict__ problems, const DevWork* __restrict__ work,
                     int32_t n_work) {
   extern __shared__ float ffma_smem[];
-  // A and B slices both [stage][k][64 + 4]: the inner loop reads four rows
-  // of A and four columns of B with one 16-B load each
-  constexpr int kSaStride = kFfmaK * kFfmaLdN, kSbStride = kFfmaK * kFfmaLdN;
+  // A slices [stage][row][32 + 4] (copied with 16-B cp.async straight from
+  // A's K-contiguous rows), B slices [stage][k][64 + 4]: per four K steps the
+  // inner loop reads four rows x four k of A and four k x four columns of B
+  // with eight 16-B loads for 64 FFMAs
+  constexpr int kSaStride = kFfmaTile * kFfmaLdK, kSbStride = kFfmaK * kFfmaLdN;
   float* sa = ffma_smem;
   float* sb = ffma_smem + kFfmaStages * kSaStride;
   const int tx = threadIdx.x & 15;  // column group
@@ -72,12 +77,19 @@ __global__ void __launch_bounds__(kFfmaThreads)
         const int st = slice % kFfmaStages, k0 = slice * kFfmaK;
         float* a = sa + st * kSaStride;
         float* b = sb + st * kSbStride;
-        // A -> [k][row] (4-B copies; consecutive threads take consecutive
-        // rows, so the shared-memory writes are conflict free), only the
-        // item's rows; the K tail is zero-filled
-        for (int e = threadIdx.x; e < kFfmaK * kFfmaTile; e += kFfmaThreads) {
-          const int r = e & (kFfmaTile - 1), kk = e / kFfmaTile, gk = k0 + kk;
-          if (r < ni) cp_async4(a + kk * kFfmaLdN + r, A + static_cast<int64_t>(i0 + r) * P.lda + min(gk, K - 1), gk < K);
+        // A -> [row][k], only the item's rows; the K tail is zero-filled
+        if (kVec) {  // 16-B copies of 4 consecutive k (8 per row and slice)
+          for (int e = threadIdx.x; e < kFfmaTile * (kFfmaK / 4); e += kFfmaThreads) {
+            const int r = e >> 3, c = (e & 7) * 4, gk = k0 + c;
+            if (r < ni)
+              cp_async16(a + r * kFfmaLdK + c, A + static_cast<int64_t>(i0 + r) * P.lda + (gk < K ? gk : 0),
+                         gk < K ? min(16, (K - gk) * 4) : 0);
+          }
+        } else {
+          for (int e = threadIdx.x; e < kFfmaK * kFfmaTile; e += kFfmaThreads) {
+            const int kk = e & (kFfmaK - 1), r = e / kFfmaK, gk = k0 + kk;
+            if (r < ni) cp_async4(a + r * kFfmaLdK + kk, A + static_cast<int64_t>(i0 + r) * P.lda + min(gk, K - 1), gk < K);
+          }
         }
         if (!bnk && kVec) {  // B [K, N] -> [k][n] in 16-B chunks (the last may run past nj: discarded columns)
           const int n4 = (nj + 3) >> 2;
@@ -113,16 +125,28 @@ __global__ void __launch_bounds__(kFfmaThreads)
       const int st = slice % kFfmaStages;
       const float* a = sa + st * kSaStride;
       const float* b = sb + st * kSbStride;
-#pragma unroll 8
-      for (int kk = 0; kk < kFfmaK; ++kk) {
-        // two 16-B shared loads per 16 FFMAs (rows ty*4.., columns tx*4..)
-        const float4 av = *reinterpret_cast<const float4*>(a + kk * kFfmaLdN + ty * 4);
-        const float4 bv = *reinterpret_cast<const float4*>(b + kk * kFfmaLdN + tx * 4);
-        const float ax[4] = {av.x, av.y, av.z, av.w}, bx[4] = {bv.x, bv.y, bv.z, bv.w};
+#pragma unroll 2
+      for (int kk = 0; kk < kFfmaK; kk += 4) {
+        // eight 16-B shared loads per 64 FFMAs: rows ty*4.. x k kk..kk+3 of A,
+        // k kk..kk+3 x columns tx*4.. of B; the k order per element stays sequential
+        float ax[4][4];
 #pragma unroll
-        for (int x = 0; x < 4; ++x)
+        for (int x = 0; x < 4; ++x) {
+          const float4 av = *reinterpret_cast<const float4*>(a + (ty * 4 + x) * kFfmaLdK + kk);
+          ax[x][0] = av.x;
+          ax[x][1] = av.y;
+          ax[x][2] = av.z;
+          ax[x][3] = av.w;
+        }
 #pragma unroll
-          for (int y = 0; y < 4; ++y) acc[x][y] = fmaf(ax[x], bx[y], acc[x][y]);
+        for (int q = 0; q < 4; ++q) {
+          const float4 bv = *reinterpret_cast<const float4*>(b + (kk + q) * kFfmaLdN + tx * 4);
+          const float bx[4] = {bv.x, bv.y, bv.z, bv.w};
+#pragma unroll
+          for (int x = 0; x < 4; ++x)
+#pragma unroll
+            for (int y = 0; y < 4; ++y) acc[x][y] = fmaf(ax[x][q], bx[y], acc[x][y]);
+        }
       }
     }
     cp_async_wait<0>();
@@ -147,7 +171,9 @@ __global__ void __launch_bounds__(kFfmaThreads)
   }
 }
 
-int ffma_smem_bytes() { return static_cast<int>(sizeof(float)) * kFfmaStages * 2 * kFfmaK * kFfmaLdN; }
+int ffma_smem_bytes() {
+  return static_cast<int>(sizeof(float)) * kFfmaStages * (kFfmaTile * kFfmaLdK + kFfmaK * kFfmaLdN);
+}
 
 // vec: every operand row 16-B aligned (base and leading dimension), so the
 // 16-B copy path is legal; the 4-B path gives bit-identical results (same
@@ -155,7 +181,7 @@ int ffma_smem_bytes() { return static_cast<int>(sizeof(float)) * kFfmaStages * 2
 cudaError_t launch_ffma(const DevProblem* problems, const DevWork* work, int32_t n_work,
                         int32_t n_ctas, cudaStream_t stream, bool vec) {
   if (n_work == 0) return cudaSuccess;
-  const int smem = ffma_smem_bytes();  // 3 x 2 x 32 x 68 floats = 51 KiB: needs the opt-in
+  const int smem = ffma_smem_bytes();  // 6 x (64 x 36 + 32 x 68) floats = 105 KiB: needs the opt-in
   cudaError_t e = vec ? configure_smem_once<ftb_ffma_kernel<true>>(smem) : configure_smem_once<ftb_ffma_kernel<false>>(smem);
   if (e != cudaSuccess) return e;
   if (vec) ftb_ffma_kernel<true><<<n_ctas, kFfmaThreads, smem, stream>>>(problems, work, n_work);
