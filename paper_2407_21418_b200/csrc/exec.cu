@@ -390,13 +390,18 @@ static void build(ExecImpl& ex, const ftb_gemm_desc* probs, const ftb_program* p
     DevWork w;
   };
   std::vector<Keyed> items;
+  static const bool prof_lower = std::getenv("FTB_PROFILE_LOWER") != nullptr;
+  double t_regions = 0, t_items = 0, t_raster = 0;
   for (int32_t p = 0; p < n; ++p) {
     const ftb_gemm_desc& d = probs[p];
     if (d.M < 1 || d.N < 1 || d.K < 1 || d.batch < 1)
       throw input_error("problem extents must be >= 1", "shape");
     if (d.op == FTB_OP_DENSE && d.batch != 1) throw input_error("dense problems have batch 1", "batch");
     int64_t covered = 0;
+    const auto tp0 = std::chrono::steady_clock::now();
     std::vector<Region> regs = plan_regions(d, progs[p], &covered);
+    const auto tp1 = std::chrono::steady_clock::now();
+    if (prof_lower) t_regions += std::chrono::duration<double, std::micro>(tp1 - tp0).count();
     const int ib = d.op == FTB_OP_BMM ? 1 : 0;  // index of i among space axes
     DevProblem P;
     std::memset(&P, 0, sizeof(P));
@@ -428,13 +433,19 @@ static void build(ExecImpl& ex, const ftb_gemm_desc* probs, const ftb_program* p
       for (int o = 0; o < 2; ++o) {
         const bool col_mn = (o == 0) && !P.b_nk;
         const int64_t gran = col_mn ? 64 : 16;
+        int64_t last_li = -1, last_lj = -1, last_cost = 0;  // consecutive regions usually share extents
         for (const Region& r : regs) {
           const int64_t li = r.hi[ib] - r.lo[ib], lj = r.hi[ib + 1] - r.lo[ib + 1];
-          const int64_t lane = o ? lj : li, col = o ? li : lj;
-          split(0, col, kMaxN, cp);
-          int64_t cols = 0;
-          for (auto& c : cp) cols += std::max<int64_t>(kMmaFloorN, round_up(c.len, gran));
-          cost[o] += ceil_div(lane, kLaneRows) * cols;
+          if (li != last_li || lj != last_lj) {
+            const int64_t lane = o ? lj : li, col = o ? li : lj;
+            split(0, col, kMaxN, cp);
+            int64_t cols = 0;
+            for (auto& c : cp) cols += std::max<int64_t>(kMmaFloorN, round_up(c.len, gran));
+            last_li = li;
+            last_lj = lj;
+            last_cost = ceil_div(lane, kLaneRows) * cols;
+          }
+          cost[o] += last_cost;
         }
       }
       swap = d.orientation >= 0 ? d.orientation : (cost[1] < cost[0] ? 1 : 0);
@@ -577,6 +588,7 @@ static void build(ExecImpl& ex, const ftb_gemm_desc* probs, const ftb_program* p
             ex.info.mma_flops += 2 * cells * kBlockK;
           }
     }
+    int64_t last_ilo = -1, last_ihi = -1, last_jlo = -1, last_jhi = -1;
     for (const Region& r : regs) {
       if (ffma) break;
       const int64_t b0 = ib ? r.lo[0] : 0, b1 = ib ? r.hi[0] : 1;
@@ -587,9 +599,17 @@ static void build(ExecImpl& ex, const ftb_gemm_desc* probs, const ftb_program* p
       if (swap) {
         split(jlo, jhi, lane_max, lp, 8);
         split(ilo, ihi, col_max, cp, 1);
+      } else if (ilo == last_ilo && ihi == last_ihi && jlo == last_jlo && jhi == last_jhi) {
+        // the same rectangle as the previous region (another batch entry): reuse its pieces
       } else {
         split(ilo, ihi, lane_max, lp, 1);
         split(jlo, jhi, col_max, cp, 8);
+      }
+      if (!swap) {
+        last_ilo = ilo;
+        last_ihi = ihi;
+        last_jlo = jlo;
+        last_jhi = jhi;
       }
       if ((P.lane_mn && lp.front().start % 8) || (P.col_mn && cp.front().start % 8))
         throw input_error("B given as [K, N] needs uKernel tiles along N that start on multiples of 8 "
@@ -626,7 +646,7 @@ static void build(ExecImpl& ex, const ftb_gemm_desc* probs, const ftb_program* p
         return e ? std::max<int64_t>(1, std::atoll(e)) : int64_t(32);
       }();
       const int64_t group = std::max<int64_t>(kMaxN, (raster_mb << 20) / kbytes / kMaxN * kMaxN);
-      std::stable_sort(items.begin() + first_item, items.end(), [group](const Keyed& a, const Keyed& b) {
+      auto raster = [group](const Keyed& a, const Keyed& b) {
         if (a.w.batch != b.w.batch) return a.w.batch < b.w.batch;
         const int64_t ga = a.w.col0 / group, gb = b.w.col0 / group;
         if (ga != gb) return ga < gb;
@@ -634,17 +654,46 @@ static void build(ExecImpl& ex, const ftb_gemm_desc* probs, const ftb_program* p
         // tiles the previous group left in L2
         if (a.w.lane0 != b.w.lane0) return (ga & 1) ? a.w.lane0 > b.w.lane0 : a.w.lane0 < b.w.lane0;
         return a.w.col0 < b.w.col0;
-      });
+      };
+      // (batched attention problems are generated in this order already)
+      const auto tr0 = std::chrono::steady_clock::now();
+      if (prof_lower) t_items += std::chrono::duration<double, std::micro>(tr0 - tp1).count();
+      if (!std::is_sorted(items.begin() + first_item, items.end(), raster))
+        std::stable_sort(items.begin() + first_item, items.end(), raster);
+      if (prof_lower) t_raster += std::chrono::duration<double, std::micro>(std::chrono::steady_clock::now() - tr0).count();
     }
     ex.info.true_flops += 2 * d.batch * d.M * d.N * d.K;
     ex.info.covered_out += covered;
     ex.info.true_out += d.batch * d.M * d.N;
   }
-  // Longest-first order so the static round-robin over persistent CTAs balances.
-  std::stable_sort(items.begin(), items.end(),
-                   [](const Keyed& a, const Keyed& b) { return a.cost > b.cost; });
-  ex.work.reserve(items.size());
-  for (auto& k : items) ex.work.push_back(k.w);
+  const auto ts0 = std::chrono::steady_clock::now();
+  // Longest-first order so the static round-robin over persistent CTAs
+  // balances. Costs take few distinct values (K blocks x MMA width), so the
+  // stable order is a counting sort over the distinct costs (O(n), the
+  // comparison sort of 35k items was the largest host cost of a C1 table).
+  {
+    std::vector<int64_t> keys;
+    keys.reserve(64);
+    for (const Keyed& k : items)
+      if (keys.empty() || keys.back() != k.cost) keys.push_back(k.cost);  // runs of equal cost collapse
+    std::sort(keys.begin(), keys.end(), std::greater<int64_t>());
+    keys.erase(std::unique(keys.begin(), keys.end()), keys.end());
+    std::vector<int64_t> start(keys.size() + 1, 0);
+    std::vector<uint32_t> bucket(items.size());
+    for (size_t i = 0; i < items.size(); ++i) {
+      const size_t b = static_cast<size_t>(
+          std::lower_bound(keys.begin(), keys.end(), items[i].cost, std::greater<int64_t>()) - keys.begin());
+      bucket[i] = static_cast<uint32_t>(b);
+      ++start[b + 1];
+    }
+    for (size_t b = 0; b < keys.size(); ++b) start[b + 1] += start[b];
+    ex.work.resize(items.size());
+    for (size_t i = 0; i < items.size(); ++i) ex.work[static_cast<size_t>(start[bucket[i]]++)] = items[i].w;
+  }
+  if (prof_lower)
+    std::fprintf(stderr, "ftb lower: regions %.0f us, items %.0f us, raster %.0f us, cost order %.0f us (%zu items)\n",
+                 t_regions, t_items, t_raster,
+                 std::chrono::duration<double, std::micro>(std::chrono::steady_clock::now() - ts0).count(), items.size());
   ex.info.n_work = static_cast<int64_t>(ex.work.size());
   ex.info.n_problems = n;
   int sms = device_sms();
