@@ -1257,6 +1257,22 @@ struct ftb_exec {
   ftb::ExecImpl impl;
 };
 
+namespace ftb {
+// While another stream of the process is being captured in torch's default
+// (global) capture mode, CUDA rejects "unsafe" calls from any thread — the
+// stream-ordered allocation and private-stream upload of a table created
+// mid-capture (e.g. a GEMM on freshly allocated graph-pool outputs inside
+// torch.cuda.graph), or the host wait on a table's upload before its launch
+// is recorded. Table create / launch / destroy switch this thread to relaxed
+// mode for their duration; none of their calls touches the capturing stream
+// except the recorded kernel launch itself.
+struct RelaxedCapture {
+  cudaStreamCaptureMode prev = cudaStreamCaptureModeRelaxed;
+  RelaxedCapture() { cudaThreadExchangeStreamCaptureMode(&prev); }
+  ~RelaxedCapture() { cudaThreadExchangeStreamCaptureMode(&prev); }
+};
+}  // namespace ftb
+
 extern "C" {
 
 int32_t ftb_device_sm_count(void) { return ftb::device_sms(); }
@@ -1265,6 +1281,7 @@ ftb_status ftb_exec_create(const ftb_gemm_desc* problems, const ftb_program* pro
                            ftb_exec** out) {
   return ftb::guarded([&] {
     if (!out || !problems || !programs) throw ftb::input_error("null argument");
+    ftb::RelaxedCapture relaxed;
     auto* ex = new ftb_exec();
     try {
       static const bool prof = std::getenv("FTB_PROFILE_CREATE") != nullptr;
@@ -1291,6 +1308,7 @@ ftb_status ftb_exec_create(const ftb_gemm_desc* problems, const ftb_program* pro
 ftb_status ftb_exec_launch(ftb_exec* ex, void* stream) {
   return ftb::guarded([&] {
     if (!ex) throw ftb::input_error("null exec");
+    ftb::RelaxedCapture relaxed;
     auto& I = ex->impl;
     cudaStream_t s = static_cast<cudaStream_t>(stream);
     std::lock_guard<std::mutex> g(I.mu);
@@ -1362,7 +1380,10 @@ ftb_status ftb_exec_export_table(const ftb_exec* ex, int32_t* out, int64_t cap, 
   });
 }
 
-void ftb_exec_destroy(ftb_exec* ex) { delete ex; }
+void ftb_exec_destroy(ftb_exec* ex) {
+  ftb::RelaxedCapture relaxed;  // e.g. an LRU eviction while a graph is being captured
+  delete ex;
+}
 
 ftb_status ftb_exec_set_trace(ftb_exec* ex, int32_t enable) {
   return ftb::guarded([&] {

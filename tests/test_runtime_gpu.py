@@ -263,3 +263,29 @@ def test_table_churn_create_launch_destroy(cuda):
     torch.cuda.synchronize()
     for A, W, C, K in jobs:
         assert close(C, A.double() @ W.double().t(), K, "churn")
+
+
+def test_tables_created_inside_a_torch_graph_capture(cuda, planner):
+    """A GEMM whose output is allocated inside torch.cuda.graph (the graph's
+    private pool: new addresses, so a new table) builds its table mid-capture
+    (relaxed capture mode for the table's own allocation and upload) and the
+    replayed graph computes the same result as eager execution."""
+    g0 = torch.Generator(device="cpu").manual_seed(3)
+    A = (torch.rand(96, 256, generator=g0) * 2 - 1).bfloat16().to(cuda)
+    W = (torch.rand(384, 256, generator=g0) * 2 - 1).bfloat16().to(cuda)
+    eager = planner.dense(A, W, b_layout="nk")
+    s = torch.cuda.Stream(cuda)
+    s.wait_stream(torch.cuda.current_stream(cuda))
+    with torch.cuda.stream(s):
+        planner.dense(A, W, b_layout="nk")
+    torch.cuda.current_stream(cuda).wait_stream(s)
+    torch.cuda.synchronize()
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g):
+        out = planner.dense(A, W, b_layout="nk")
+        out2 = torch.relu(out)
+    out.zero_()
+    g.replay()
+    torch.cuda.synchronize()
+    assert torch.equal(out, eager)
+    assert torch.equal(out2, torch.relu(eager))
