@@ -219,8 +219,14 @@ class Executable:
         s = stream if stream is not None else torch.cuda.current_stream(self.device)
         if s.device != self.device:
             raise ValueError(f"stream is on {s.device}, the table on {self.device}")
-        with torch.cuda.device(self.device):
-            _lib.check(_lib.lib().ftb_exec_launch(self._h, C.c_void_p(s.cuda_stream)))
+        fn = _lib.lib().ftb_exec_launch
+        if torch.cuda.current_device() == self.device.index:  # the common case: no device switch needed
+            st = fn(self._h, C.c_void_p(s.cuda_stream))
+        else:
+            with torch.cuda.device(self.device):
+                st = fn(self._h, C.c_void_p(s.cuda_stream))
+        if st:
+            _lib.check(st)
 
     def config(self) -> dict:
         """Pipeline shape chosen for this table (tcgen05 kernel)."""

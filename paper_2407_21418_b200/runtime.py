@@ -142,6 +142,7 @@ class Planner:
         self._hw_key = json.dumps(self.hw.to_doc(), sort_keys=True)
         self._cache: dict[tuple, PlanRecord] = {}
         self._exe_cache: dict[tuple, Executable] = {}  # insertion-ordered LRU of lowered tables
+        self._op_plans: dict[tuple, PlanRecord] = {}   # (op, extents, ...) -> plan: skips instance building on hits
         self.exe_cache_size = 32
         self._lock = threading.Lock()
 
@@ -225,9 +226,12 @@ class Planner:
         M, K = A.shape
         N = B.shape[1] if b_layout == "kn" else B.shape[0]
         fp32 = A.dtype == torch.float32
-        inst = dense_instance(M, N, K, elem_bytes=4 if fp32 else 2)
-        planner = self if (not fp32 or not self.hw.tcgen05_mode) else _ffma_planner()
-        rec = planner.plan([inst])[0]
+        rec = self._op_plans.get(("dense", M, N, K, fp32))
+        if rec is None:
+            inst = dense_instance(M, N, K, elem_bytes=4 if fp32 else 2)
+            planner = self if (not fp32 or not self.hw.tcgen05_mode) else _ffma_planner()
+            rec = planner.plan([inst])[0]
+            self._op_plans[("dense", M, N, K, fp32)] = rec
         if out is None:
             out = torch.empty(M, N, dtype=torch.float32 if fp32 else torch.bfloat16, device=A.device)
         return self._launch(rec, A, B, out, b_layout, bias, activation, stream)
@@ -237,7 +241,11 @@ class Planner:
 
         b, M, K = A.shape
         N = B.shape[2] if b_layout == "kn" else B.shape[1]
-        rec = self.plan([bmm_instance(b, M, N, K, dynamic)])[0]
+        key = ("bmm", b, M, N, K, tuple(dynamic))
+        rec = self._op_plans.get(key)
+        if rec is None:
+            rec = self.plan([bmm_instance(b, M, N, K, dynamic)])[0]
+            self._op_plans[key] = rec
         if out is None:
             out = torch.empty(b, M, N, dtype=torch.bfloat16, device=A.device)
         return self._launch(rec, A, B, out, b_layout, stream=stream)
