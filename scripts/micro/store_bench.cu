@@ -117,6 +117,15 @@ __global__ void __launch_bounds__(192, 1) store_kernel(const __grid_constant__ M
             tma_store_3d(&maps.s128w, smem_addr(box), col0 + c0, static_cast<int>(row0), 0);
             bulk_commit();
           }
+        } else if (mode == 5) {
+          // LSU, coalesced: per instruction 4 rows x 128 B (8 lanes per row), 8 instructions per
+          // 32 x 64 group (the register contents stand in for a staged-and-reread box)
+#pragma unroll
+          for (int q = 0; q < 8; ++q) {
+            const int row = q * 4 + (lane >> 3), cc = (lane & 7) * 8;
+            __nv_bfloat16* dst = C + (row0 + warp * 32 + row) * ldc + col0 + c0 + cc;
+            __stcg(reinterpret_cast<uint4*>(dst), make_uint4(r[q * 4], r[q * 4 + 1], r[q * 4 + 2], r[q * 4 + 3]));
+          }
         } else {
           // LSU: each lane writes its own row's 64 columns (8 x 16 B) straight from registers
           __nv_bfloat16* dst = C + (row0 + warp * 32 + lane) * ldc + col0 + c0;
@@ -173,10 +182,10 @@ int main() {
   const int smem = 32768 + 4 * 49152 + 1024 + 256;
   cudaFuncSetAttribute(store_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   const char* names[] = {"2KiB boxes {32x32} SW64 (current)", "4KiB boxes {64x32} SW128 per warp", "16KiB boxes {64x128} SW128 per CTA",
-                         "-", "LSU st.global.v4 per-lane rows"};
+                         "-", "LSU st.global.v4 per-lane rows", "LSU st.global.v4 coalesced 4 rows x 128 B"};
   for (int items : {1, 16}) {
     for (int load : {0, 1}) {
-      for (int mode : {0, 1, 2, 4}) {
+      for (int mode : {0, 1, 2, 4, 5}) {
         store_kernel<<<ctas, 192, smem>>>(m, items, mode, load, (__nv_bfloat16*)c, ldc, out, wrap);
         cudaDeviceSynchronize();
         cudaEvent_t e0, e1;
