@@ -473,3 +473,61 @@ def test_overflow_split_bitwise(cuda, monkeypatch, M, N, K, grows):
     assert torch.equal(outs[0], outs[1])
     assert (items[1] > items[0]) == grows, items
     assert_close(outs[1], ref, K, f"M{M} N{N} K{K}")
+
+
+@pytest.mark.parametrize("M,N,K,compact", [(160, 772, 768, False), (160, 771, 768, True), (352, 2312, 768, False),
+                                           (1, 1000, 4096, False)])
+@pytest.mark.parametrize("switch", ["FTB_COLSPLIT_MIN=128", "FTB_PARAM_MAPS=0", "FTB_TMA_TAIL=0"])
+def test_round2_lowering_switches_bitwise(cuda, monkeypatch, M, N, K, compact, switch):
+    """Round-2 lowering paths against their switched-off forms, bit for bit:
+    32/64-column pieces of one-wave tables (vs 128), descriptors in the
+    kernel parameter (vs the table copy), TMA stores up to N rounded down to
+    8 with element tails (vs predicated stores) — on row lengths that are
+    not a multiple of 8 (padded and compact C), with the padding / guard
+    elements untouched."""
+    from paper_2407_21418_b200.runtime import Planner, dense_instance
+
+    g = torch.Generator(device="cpu").manual_seed(M * 7 + N)
+    A = (torch.rand(M, K, generator=g) * 2 - 1).bfloat16().to(cuda)
+    B = (torch.rand(N, K, generator=g) * 2 - 1).bfloat16().to(cuda)
+    ref = A.double() @ B.double().t()
+    prog = Planner().plan([dense_instance(M, N, K)])[0].program
+    ld = N if compact else (N + 7) // 8 * 8
+    key, val = switch.split("=")
+    outs = []
+    for on in (True, False):
+        if on:
+            monkeypatch.delenv(key, raising=False)
+        else:
+            monkeypatch.setenv(key, val)
+        buf = torch.full((M * ld + 64,), float("nan"), dtype=torch.bfloat16, device=cuda)
+        C = buf[:M * ld].view(M, ld)[:, :N]
+        ex = Executable([gemm_desc(A, B, C, "nk")], [prog])
+        ex.launch()
+        torch.cuda.synchronize()
+        assert torch.isnan(buf[M * ld:].float()).all()
+        if not compact:
+            assert torch.isnan(buf[:M * ld].view(M, ld)[:, N:].float()).all(), "row padding written"
+        outs.append(C.clone())
+        ex.close()
+    assert torch.equal(outs[0], outs[1])
+    assert_close(outs[0], ref, K, f"M{M} N{N} K{K}")
+
+
+@pytest.mark.parametrize("b,M,N,K", [(3, 53, 77, 768), (2, 130, 64, 100)])
+def test_ffma_bmm_merged_rectangles(cuda, b, M, N, K):
+    """FFMA mode on a batched problem with ragged tiles: the merged-rectangle
+    lowering (whole uKernel rectangles per <= 64 x 64 CTA) covers every
+    element of every batch entry (per-element fp32 tolerance)."""
+    from paper_2407_21418_b200.mktune.hardware import b200_ffma
+    from paper_2407_21418_b200.runtime import Planner, bmm_instance
+
+    g = torch.Generator(device="cpu").manual_seed(b * M)
+    A = (torch.rand(b, M, K, generator=g) * 2 - 1).to(cuda)
+    Bm = (torch.rand(b, K, N, generator=g) * 2 - 1).to(cuda)
+    C = torch.full((b, M, N), float("nan"), device=cuda)
+    prog = Planner(hw=b200_ffma()).plan([bmm_instance(b, M, N, K)])[0].program
+    ex = Executable([gemm_desc(A, Bm, C, "kn")], [prog])
+    ex.launch()
+    torch.cuda.synchronize()
+    assert_close(C, A.double() @ Bm.double(), K, "ffma bmm", ffma=True)
