@@ -218,6 +218,14 @@ class Planner:
                 self._exe_cache.pop(next(iter(self._exe_cache)))
         return out
 
+    def _memo_op(self, key, rec) -> None:
+        """Bounded memo of the op entry points (the plan cache itself stays
+        complete): a serving process with unbounded shape variety does not
+        grow it without limit."""
+        if len(self._op_plans) >= 65536:
+            self._op_plans.clear()
+        self._op_plans[key] = rec
+
     def dense(self, A, B, b_layout: str = "kn", out=None, stream=None, bias=None, activation=None):
         """C = act(A @ B + bias) (B as [K,N] for "kn", as nn.Linear weight [N,K]
         for "nk"); bias [N] and activation ("gelu") are fused into the epilogue."""
@@ -231,7 +239,7 @@ class Planner:
             inst = dense_instance(M, N, K, elem_bytes=4 if fp32 else 2)
             planner = self if (not fp32 or not self.hw.tcgen05_mode) else _ffma_planner()
             rec = planner.plan([inst])[0]
-            self._op_plans[("dense", M, N, K, fp32)] = rec
+            self._memo_op(("dense", M, N, K, fp32), rec)
         if out is None:
             out = torch.empty(M, N, dtype=torch.float32 if fp32 else torch.bfloat16, device=A.device)
         return self._launch(rec, A, B, out, b_layout, bias, activation, stream)
@@ -245,7 +253,7 @@ class Planner:
         rec = self._op_plans.get(key)
         if rec is None:
             rec = self.plan([bmm_instance(b, M, N, K, dynamic)])[0]
-            self._op_plans[key] = rec
+            self._memo_op(key, rec)
         if out is None:
             out = torch.empty(b, M, N, dtype=torch.bfloat16, device=A.device)
         return self._launch(rec, A, B, out, b_layout, stream=stream)
